@@ -1,0 +1,124 @@
+// Device-side primitives shared by the HyKKT kernels: acquire/release
+// flags, a sense-reversing grid barrier for cooperative persistent kernels,
+// bounded spin-waits (a logic error must never hang the GPU), warp and
+// block reductions with a fixed combination order (deterministic results).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hykkt::dev {
+
+// Spin budget: ~2^31 cycles (> 1 s at 1.9 GHz) before a waiter gives up,
+// raises the abort flag and lets every other waiter fall through.
+constexpr long long kSpinBudget = 1ll << 31;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Values produced by other SMs inside the same launch are read through L2
+// (ld.global.cg); L1 is not coherent across SMs.
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ void stcg(double* p, double v) { __stcg(p, v); }
+
+// Waits until *flag == want. Returns false (and raises *abort) on timeout
+// or when another waiter already aborted.
+__device__ __forceinline__ bool wait_flag(const int* flag, int want, int* abort) {
+  if (ld_acquire(flag) == want) return true;
+  const long long t0 = clock64();
+  unsigned ns = 20;
+  for (;;) {
+    if (ld_acquire(flag) == want) return true;
+    if (ld_relaxed(abort)) return false;
+    if (clock64() - t0 > kSpinBudget) {
+      atomicExch(abort, 1);
+      return false;
+    }
+    __nanosleep(ns);
+    if (ns < 200) ns += 20;
+  }
+}
+
+struct GridBarrier {
+  unsigned* count;
+  unsigned* gen;
+};
+
+// Sense-reversing barrier over all blocks of a cooperative launch.
+__device__ __forceinline__ void grid_sync(const GridBarrier& b, int* abort) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = ld_acquire(b.gen);
+    __threadfence();
+    const unsigned arrived = atomicAdd(b.count, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(b.count, 0u);
+      __threadfence();
+      st_release(b.gen, g + 1);
+    } else {
+      const long long t0 = clock64();
+      while (ld_acquire(b.gen) == g) {
+        if (ld_relaxed(abort) || clock64() - t0 > kSpinBudget) {
+          atomicExch(abort, 1);
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block sum with a fixed order (warp tree, then warp 0 over warp partials).
+// `scratch` holds >= 32 doubles of shared memory. Result valid in all threads.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double t = (lane < nw) ? scratch[lane] : 0.0;
+  if (wid == 0) {
+    t = warp_sum(t);
+    if (lane == 0) scratch[32] = t;
+  }
+  __syncthreads();
+  const double r = scratch[32];
+  __syncthreads();
+  return r;
+}
+
+// Non-negative doubles order like their bit patterns: exact max via atomics.
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+}  // namespace hykkt::dev

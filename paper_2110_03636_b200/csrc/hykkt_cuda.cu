@@ -1,0 +1,979 @@
+// B200 (sm_100a) HyKKT device context and the C ABI declared in
+// include/hykkt.h.
+//
+// Per interior-method iteration the whole of solve_full's numeric work
+// (proj/core/src/solver.cpp:295-328: reduce, ruiz_scale, assemble_h_gamma,
+// factorize_with_ladder, w solve, cg_schur with the delta2 restart, dx
+// solve, unscale, recover) runs on the handle's stream from values resident
+// in HBM.  The host only makes the ladder decision per factorization
+// attempt and reads the CG outcome; the CG loop itself is one cooperative
+// persistent kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hykkt.h"
+#include "analyze.hpp"
+#include "host_metrics.hpp"
+#include "kernels_assemble.cuh"
+#include "kernels_solve.cuh"
+
+namespace hykkt {
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+struct StateError : std::runtime_error {
+  explicit StateError(const std::string& w) : std::runtime_error(w) {}
+};
+struct TimeoutError : std::runtime_error {
+  explicit TimeoutError(const std::string& w) : std::runtime_error(w) {}
+};
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t e_ = (x);                                                      \
+    if (e_ != cudaSuccess)                                                     \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(std::size_t count) {
+    if (count == n && p) return;
+    reset();
+    n = count;
+    CK(cudaMalloc(&p, std::max<std::size_t>(count, 1) * sizeof(T)));
+  }
+  void upload(const T* src, std::size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) CK(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+};
+
+template <typename A>
+std::vector<int> to_i32(const std::vector<A>& v) {
+  return std::vector<int>(v.begin(), v.end());
+}
+
+constexpr int kThreads = 256;
+int blocks_for(long long n) { return static_cast<int>(std::max<long long>(1, (n + kThreads - 1) / kThreads)); }
+
+// Per-launch status block read back after each decision point.
+struct StatusBlock {
+  int fail_col;
+  int abort;
+  int ruiz_sweeps;
+  int pad;
+  dev::CgResultDev cg;
+};
+
+}  // namespace
+
+}  // namespace hykkt
+
+struct hykkt_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  int coop_factor_blocks = 0, coop_trsv_blocks = 0, coop_cg_blocks = 0, coop_ruiz_blocks = 0;
+
+  bool have_plan = false, have_kkt = false, have_values = false, have_factor = false;
+  hykkt::SupernodalPlan sp;
+  hykkt::KktPlan kp;
+
+  // device supernodal plan
+  hykkt::DBuf<int> order, first, nrows, off, rows_ptr, rows, parent, child_ptr, child;
+  hykkt::DBuf<int> upd_ptr, upd_d, upd_off, upd_cnt, lrow_ptr, lrow_col, lrow_pos;
+  hykkt::DBuf<int> perm, iperm, src_to_panel, src_row, src_col;
+  hykkt::DBuf<double> panel, y, src_vals, bvec, xvec;
+  hykkt::DBuf<int> fdone, bdone, fac_done;
+  hykkt::DBuf<unsigned> barrier;  // count, gen
+  hykkt::DBuf<hykkt::StatusBlock> status;
+  int epoch = 0;
+
+  // KKT plan arrays
+  hykkt::DBuf<int> ht_row, ht_col, ht_hsrc, ht_pp, ht_pa, ht_pb, ht_pk;
+  hykkt::DBuf<int> hg_row, hg_col, hg_src, hg_pp, hg_pa, hg_pb;
+  hykkt::DBuf<int> j_cp, j_ri, j_col, jcsr_src, jcsr_rp, jcsr_ci_perm;
+  hykkt::DBuf<int> jd_cp, jd_ri, jdcsr_rp, jdcsr_ci, jdcsr_src;
+  // values
+  hykkt::DBuf<double> hval, jval, jdval, d_x, d_s, r_tx, r_s, r_y, r_yd;
+  // work
+  hykkt::DBuf<double> ht, hts, js, js_csr, r_x, rxs, rys, dscale, norms, hg, rhat, maxdiag;
+  hykkt::DBuf<int> ruiz_flags;
+  hykkt::DBuf<double> cg_rhs, cg_x, cg_r, cg_p, cg_q, partials;
+  hykkt::DBuf<double> dx_s, dx, dy, ds, dyd;
+
+  hykkt_timing_t timing{};
+  long long launches = 0;
+
+  hykkt::dev::SnPlan snplan() const {
+    hykkt::dev::SnPlan s;
+    s.n = static_cast<int>(sp.n);
+    s.nsup = static_cast<int>(sp.nsup);
+    s.order = order.p;
+    s.first = first.p;
+    s.nrows = nrows.p;
+    s.off = off.p;
+    s.rows_ptr = rows_ptr.p;
+    s.rows = rows.p;
+    s.parent = parent.p;
+    s.child_ptr = child_ptr.p;
+    s.child = child.p;
+    s.upd_ptr = upd_ptr.p;
+    s.upd_d = upd_d.p;
+    s.upd_off = upd_off.p;
+    s.upd_cnt = upd_cnt.p;
+    s.lrow_ptr = lrow_ptr.p;
+    s.lrow_col = lrow_col.p;
+    s.lrow_pos = lrow_pos.p;
+    s.perm = perm.p;
+    s.iperm = iperm.p;
+    return s;
+  }
+
+  hykkt::dev::AsmPlan asmplan() const {
+    hykkt::dev::AsmPlan a;
+    a.nx = static_cast<int>(kp.nx);
+    a.mc = static_cast<int>(kp.mc);
+    a.md = static_cast<int>(kp.md);
+    a.n_ht = static_cast<int>(kp.ht.nnz());
+    a.ht_row = ht_row.p;
+    a.ht_col = ht_col.p;
+    a.ht_hsrc = ht_hsrc.p;
+    a.ht_pp = ht_pp.p;
+    a.ht_pa = ht_pa.p;
+    a.ht_pb = ht_pb.p;
+    a.ht_pk = ht_pk.p;
+    a.n_hg = static_cast<int>(kp.hg.nnz());
+    a.hg_row = hg_row.p;
+    a.hg_col = hg_col.p;
+    a.hg_src = hg_src.p;
+    a.hg_pp = hg_pp.p;
+    a.hg_pa = hg_pa.p;
+    a.hg_pb = hg_pb.p;
+    a.nnz_j = static_cast<int>(kp.j.nnz());
+    a.j_cp = j_cp.p;
+    a.j_ri = j_ri.p;
+    a.j_col = j_col.p;
+    a.jcsr_src = jcsr_src.p;
+    a.nnz_jd = static_cast<int>(kp.jd.nnz());
+    a.jd_cp = jd_cp.p;
+    a.jd_ri = jd_ri.p;
+    return a;
+  }
+};
+
+namespace hykkt {
+namespace {
+
+using Ctx = hykkt_context;
+
+void coop_launch(Ctx& c, const void* fn, int blocks, void* args) {
+  void* argv[] = {args};
+  CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), argv, 0, c.stream));
+  c.launches++;
+}
+
+void check_launch(Ctx& c) {
+  CK(cudaGetLastError());
+  c.launches++;
+}
+
+int occupancy_blocks(Ctx& c, const void* fn) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+  return std::max(1, per_sm) * c.num_sms;
+}
+
+void init_ctx(Ctx& c, int device) {
+  c.device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  CK(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+  int coop = 0;
+  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  if (!coop) throw CudaError("device does not support cooperative launch");
+  c.coop_factor_blocks = occupancy_blocks(c, (const void*)dev::k_factor);
+  c.coop_trsv_blocks = occupancy_blocks(c, (const void*)dev::k_trsv);
+  c.coop_cg_blocks = occupancy_blocks(c, (const void*)dev::k_cg);
+  c.coop_ruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_ruiz), 2 * c.num_sms);
+  c.barrier.alloc(2);
+  CK(cudaMemsetAsync(c.barrier.p, 0, 2 * sizeof(unsigned), c.stream));
+  c.status.alloc(1);
+  CK(cudaMemsetAsync(c.status.p, 0, sizeof(StatusBlock), c.stream));
+}
+
+void upload_plan(Ctx& c, const CscPattern& src_pattern) {
+  const SupernodalPlan& s = c.sp;
+  cudaStream_t st = c.stream;
+  c.order.upload(s.order, st);
+  c.first.upload(s.sn_first, st);
+  c.nrows.upload(s.sn_nrows, st);
+  c.off.upload(to_i32(s.sn_off), st);
+  c.rows_ptr.upload(s.sn_rows_ptr, st);
+  c.rows.upload(s.sn_rows, st);
+  c.parent.upload(s.sn_parent, st);
+  c.child_ptr.upload(s.child_ptr, st);
+  c.child.upload(s.child, st);
+  c.upd_ptr.upload(s.upd_ptr, st);
+  c.upd_d.upload(s.upd_d, st);
+  c.upd_off.upload(s.upd_off, st);
+  c.upd_cnt.upload(s.upd_cnt, st);
+  c.lrow_ptr.upload(s.lrow_ptr, st);
+  c.lrow_col.upload(s.lrow_col, st);
+  c.lrow_pos.upload(s.lrow_pos, st);
+  c.perm.upload(to_i32(s.perm), st);
+  c.iperm.upload(to_i32(s.iperm), st);
+  c.src_to_panel.upload(s.src_to_panel, st);
+  std::vector<int> srow(src_pattern.nnz()), scol(src_pattern.nnz());
+  for (idx j = 0; j < src_pattern.ncols; ++j) {
+    for (idx p = src_pattern.cp[j]; p < src_pattern.cp[j + 1]; ++p) {
+      srow[p] = static_cast<int>(src_pattern.ri[p]);
+      scol[p] = static_cast<int>(j);
+    }
+  }
+  c.src_row.upload(srow, st);
+  c.src_col.upload(scol, st);
+  c.panel.alloc(s.panel_size);
+  c.y.alloc(s.n);
+  c.bvec.alloc(s.n);
+  c.xvec.alloc(s.n);
+  c.fdone.alloc(s.nsup);
+  c.bdone.alloc(s.nsup);
+  c.fac_done.alloc(s.nsup);
+  CK(cudaMemsetAsync(c.fdone.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
+  CK(cudaMemsetAsync(c.bdone.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
+  CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
+  c.epoch = 0;
+  c.have_plan = true;
+  c.have_factor = false;
+}
+
+StatusBlock read_status(Ctx& c) {
+  StatusBlock sb;
+  CK(cudaMemcpyAsync(&sb, c.status.p, sizeof(sb), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  if (sb.abort) {
+    throw TimeoutError("device wait timed out (dependency deadlock or lost wake-up); results discarded");
+  }
+  return sb;
+}
+
+void reset_fail(Ctx& c) {
+  // fail_col = INT_MAX-ish (0x7f7f7f7f), abort = 0
+  CK(cudaMemsetAsync(&c.status.p->fail_col, 0x7f, sizeof(int), c.stream));
+  CK(cudaMemsetAsync(&c.status.p->abort, 0, sizeof(int), c.stream));
+}
+
+// One factorization attempt on the values in c.src_vals (KKT: H_gamma
+// slots), shifted by delta1.  Returns failed column or -1.
+int factor_attempt(Ctx& c, const double* src, double delta1, double floor_abs,
+                   const double* maxdiag, double floor_rel) {
+  const SupernodalPlan& s = c.sp;
+  CK(cudaMemsetAsync(c.panel.p, 0, sizeof(double) * std::max<idx>(1, s.panel_size), c.stream));
+  const int nsrc = static_cast<int>(s.src_to_panel.size());
+  if (nsrc > 0) {
+    dev::k_scatter<<<blocks_for(nsrc), kThreads, 0, c.stream>>>(
+        nsrc, src, c.src_to_panel.p, c.src_row.p, c.src_col.p, delta1, c.panel.p);
+    check_launch(c);
+  }
+  reset_fail(c);
+  dev::FactorArgs fa;
+  fa.s = c.snplan();
+  fa.panel = c.panel.p;
+  fa.done = c.fac_done.p;
+  fa.epoch = ++c.epoch;
+  fa.floor_abs = floor_abs;
+  fa.maxdiag = maxdiag;
+  fa.floor_rel = floor_rel;
+  fa.fail_col = &c.status.p->fail_col;
+  fa.abort = &c.status.p->abort;
+  if (s.nsup > 0) coop_launch(c, (const void*)dev::k_factor, c.coop_factor_blocks, &fa);
+  const StatusBlock sb = read_status(c);
+  return sb.fail_col >= static_cast<int>(s.n) ? -1 : sb.fail_col;
+}
+
+void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, double* x_out) {
+  const SupernodalPlan& s = c.sp;
+  if (s.nsup == 0) return;
+  dev::TrsvArgs ta;
+  ta.s = c.snplan();
+  ta.panel = c.panel.p;
+  ta.y = c.y.p;
+  ta.x_out = x_out;
+  ta.fdone = c.fdone.p;
+  ta.bdone = c.bdone.p;
+  ta.epoch = ++c.epoch;
+  ta.abort = &c.status.p->abort;
+  ta.rhs.b = b;
+  ta.rhs.u = u;
+  ta.rhs.j_cp = c.j_cp.p;
+  ta.rhs.j_ri = c.j_ri.p;
+  ta.rhs.jval = jval;
+  coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
+}
+
+dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
+  dev::CgArgs a;
+  a.tr.s = c.snplan();
+  a.tr.panel = c.panel.p;
+  a.tr.y = c.y.p;
+  a.tr.x_out = nullptr;
+  a.tr.fdone = c.fdone.p;
+  a.tr.bdone = c.bdone.p;
+  a.tr.epoch = 0;
+  a.tr.abort = &c.status.p->abort;
+  a.tr.rhs.b = nullptr;
+  a.tr.rhs.u = c.cg_p.p;
+  a.tr.rhs.j_cp = c.j_cp.p;
+  a.tr.rhs.j_ri = c.j_ri.p;
+  a.tr.rhs.jval = c.js.p;
+  a.mc = static_cast<int>(c.kp.mc);
+  a.jcsr_rp = c.jcsr_rp.p;
+  a.jcsr_ci_perm = c.jcsr_ci_perm.p;
+  a.jcsr = c.js_csr.p;
+  a.rhs = c.cg_rhs.p;
+  a.x = c.cg_x.p;
+  a.r = c.cg_r.p;
+  a.p = c.cg_p.p;
+  a.q = c.cg_q.p;
+  a.partials = c.partials.p;
+  a.delta2 = delta2;
+  a.tol = cfg.cg_tol;
+  a.thr = cfg.small_quadratic_threshold;
+  a.max_iter = cfg.cg_max_iter;
+  a.epoch_base = c.epoch;
+  a.res = &c.status.p->cg;
+  a.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+  if (c.sp.nsup == 0 && c.kp.mc > 0) throw StateError("empty factor with constraints");
+  coop_launch(c, (const void*)dev::k_cg, c.coop_cg_blocks, &a);
+  c.epoch += static_cast<int>(std::min<long long>(cfg.cg_max_iter, 1 << 28)) + 1;
+  return read_status(c).cg;
+}
+
+void validate_cfg(const hykkt_config_t& cfg) {
+  if (cfg.gamma < 0.0) throw InvalidArgument("gamma must be >= 0");
+  if (!(cfg.delta_min > 0.0) || !(cfg.delta_max > 0.0) || cfg.delta_min > cfg.delta_max)
+    throw InvalidArgument("need 0 < delta_min <= delta_max");
+  if (cfg.delta2 < 0.0) throw InvalidArgument("delta2 must be >= 0");
+  if (!(cfg.cg_tol > 0.0)) throw InvalidArgument("cg_tol must be positive");
+  if (cfg.cg_max_iter <= 0) throw InvalidArgument("cg_max_iter must be > 0");
+  if (!(cfg.small_quadratic_threshold > 0.0)) throw InvalidArgument("small_quadratic_threshold must be positive");
+  if (!(cfg.pivot_floor > 0.0)) throw InvalidArgument("pivot_floor must be positive");
+  if (!(cfg.ruiz_tol > 0.0)) throw InvalidArgument("ruiz_tol must be positive");
+  if (cfg.ruiz_max_iters <= 0) throw InvalidArgument("ruiz_max_iters must be > 0");
+}
+
+CscPattern pattern_from(idx nrows, idx ncols, const std::int64_t* cp, const std::int64_t* ri) {
+  if (!cp) throw InvalidArgument("null column pointer");
+  CscPattern p;
+  p.nrows = nrows;
+  p.ncols = ncols;
+  p.cp.assign(cp, cp + ncols + 1);
+  if (p.cp.back() < 0) throw InvalidArgument("col_ptr must start at 0 and end at nnz");
+  if (p.cp.back() > 0 && !ri) throw InvalidArgument("null row index array");
+  p.ri.assign(ri, ri + p.cp.back());
+  return p;
+}
+
+void analyze_kkt(Ctx& c, idx nx, idx mc, idx md, const std::int64_t* hcp, const std::int64_t* hri,
+                 const std::int64_t* jcp, const std::int64_t* jri, const std::int64_t* jdcp,
+                 const std::int64_t* jdri, const std::int64_t* perm) {
+  if (nx < 0 || mc < 0 || md < 0) throw InvalidArgument("negative dimension");
+  if (nx >= (idx{1} << 30) || mc >= (idx{1} << 30) || md >= (idx{1} << 30)) throw InvalidArgument("dimension too large");
+  CscPattern h = pattern_from(nx, nx, hcp, hri);
+  CscPattern j = pattern_from(mc, nx, jcp, jri);
+  CscPattern jd = pattern_from(md, nx, jdcp, jdri);
+  c.kp = build_kkt_plan(nx, mc, md, h, j, jd);
+  std::vector<idx> pv;
+  if (perm) pv.assign(perm, perm + nx);
+  c.sp = build_supernodal_plan(c.kp.hg, std::move(pv));
+  upload_plan(c, c.kp.hg);
+  const KktPlan& k = c.kp;
+  cudaStream_t st = c.stream;
+  std::vector<int> htc(k.ht.nnz()), hgc(k.hg.nnz());
+  for (idx col = 0; col < nx; ++col) {
+    for (idx p = k.ht.cp[col]; p < k.ht.cp[col + 1]; ++p) htc[p] = static_cast<int>(col);
+    for (idx p = k.hg.cp[col]; p < k.hg.cp[col + 1]; ++p) hgc[p] = static_cast<int>(col);
+  }
+  c.ht_row.upload(to_i32(k.ht.ri), st);
+  c.ht_col.upload(htc, st);
+  c.ht_hsrc.upload(k.ht_hsrc, st);
+  c.ht_pp.upload(k.ht_prod_ptr, st);
+  c.ht_pa.upload(k.ht_prod_a, st);
+  c.ht_pb.upload(k.ht_prod_b, st);
+  c.ht_pk.upload(k.ht_prod_k, st);
+  c.hg_row.upload(to_i32(k.hg.ri), st);
+  c.hg_col.upload(hgc, st);
+  c.hg_src.upload(k.hg_htsrc, st);
+  c.hg_pp.upload(k.hg_prod_ptr, st);
+  c.hg_pa.upload(k.hg_prod_a, st);
+  c.hg_pb.upload(k.hg_prod_b, st);
+  std::vector<int> jcol(k.j.nnz());
+  for (idx col = 0; col < nx; ++col) {
+    for (idx p = k.j.cp[col]; p < k.j.cp[col + 1]; ++p) jcol[p] = static_cast<int>(col);
+  }
+  c.j_cp.upload(to_i32(k.j.cp), st);
+  c.j_ri.upload(to_i32(k.j.ri), st);
+  c.j_col.upload(jcol, st);
+  c.jcsr_src.upload(k.jcsr_src, st);
+  c.jcsr_rp.upload(k.j_rp, st);
+  std::vector<int> ci_perm(k.j_ci.size());
+  for (std::size_t e = 0; e < ci_perm.size(); ++e) ci_perm[e] = static_cast<int>(c.sp.iperm[k.j_ci[e]]);
+  c.jcsr_ci_perm.upload(ci_perm, st);
+  c.jd_cp.upload(to_i32(k.jd.cp), st);
+  c.jd_ri.upload(to_i32(k.jd.ri), st);
+  c.jdcsr_rp.upload(k.jd_rp, st);
+  c.jdcsr_ci.upload(k.jd_ci, st);
+  c.jdcsr_src.upload(k.jdcsr_src, st);
+  // work buffers
+  c.hval.alloc(k.h.nnz());
+  c.jval.alloc(k.j.nnz());
+  c.jdval.alloc(k.jd.nnz());
+  c.d_x.alloc(nx);
+  c.d_s.alloc(md);
+  c.r_tx.alloc(nx);
+  c.r_s.alloc(md);
+  c.r_y.alloc(mc);
+  c.r_yd.alloc(md);
+  c.ht.alloc(k.ht.nnz());
+  c.hts.alloc(k.ht.nnz());
+  c.js.alloc(k.j.nnz());
+  c.js_csr.alloc(k.j.nnz());
+  c.r_x.alloc(nx);
+  c.rxs.alloc(nx);
+  c.rys.alloc(mc);
+  c.dscale.alloc(nx + mc);
+  c.norms.alloc(nx + mc);
+  c.hg.alloc(k.hg.nnz());
+  c.rhat.alloc(nx);
+  c.maxdiag.alloc(1);
+  c.cg_rhs.alloc(mc);
+  c.cg_x.alloc(mc);
+  c.cg_r.alloc(mc);
+  c.cg_p.alloc(mc);
+  c.cg_q.alloc(mc);
+  c.partials.alloc(4 * static_cast<std::size_t>(std::max(c.coop_cg_blocks, 1)));
+  c.dx_s.alloc(nx);
+  c.dx.alloc(nx);
+  c.dy.alloc(mc);
+  c.ds.alloc(md);
+  c.dyd.alloc(md);
+  CK(cudaStreamSynchronize(st));
+  c.have_kkt = true;
+  c.have_values = false;
+}
+
+void upload_values(Ctx& c, const hykkt_values_t* v) {
+  if (!c.have_kkt) throw StateError("hykkt_analyze must be called first");
+  if (!v) throw InvalidArgument("null values");
+  const KktPlan& k = c.kp;
+  cudaStream_t st = c.stream;
+  auto up = [&](hykkt::DBuf<double>& b, const double* src, idx n, const char* name) {
+    if (n > 0 && !src) throw InvalidArgument(std::string("null ") + name);
+    if (n > 0) CK(cudaMemcpyAsync(b.p, src, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  };
+  up(c.hval, v->h_val, k.h.nnz(), "h_val");
+  up(c.jval, v->j_val, k.j.nnz(), "j_val");
+  up(c.jdval, v->jd_val, k.jd.nnz(), "jd_val");
+  up(c.d_x, v->d_x, k.nx, "d_x");
+  up(c.d_s, v->d_s, k.md, "d_s");
+  up(c.r_tx, v->r_tilde_x, k.nx, "r_tilde_x");
+  up(c.r_s, v->r_s, k.md, "r_s");
+  up(c.r_y, v->r_y, k.mc, "r_y");
+  up(c.r_yd, v->r_yd, k.md, "r_yd");
+  c.have_values = true;
+}
+
+struct Events {
+  cudaEvent_t e[6] = {};
+  bool on = false;
+  void create() {
+    for (auto& x : e) CK(cudaEventCreate(&x));
+    on = true;
+  }
+  void rec(int i, cudaStream_t s) {
+    if (on) CK(cudaEventRecord(e[i], s));
+  }
+  ~Events() {
+    for (auto& x : e) if (x) cudaEventDestroy(x);
+  }
+};
+
+void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int flags,
+                    hykkt_report_t* rep) {
+  if (!c.have_values) throw StateError("no values uploaded");
+  validate_cfg(cfg);
+  const KktPlan& k = c.kp;
+  const dev::AsmPlan ap = c.asmplan();
+  cudaStream_t st = c.stream;
+  const long long launches0 = c.launches;
+  Events ev;
+  if (flags & HYKKT_FLAG_TIMING) ev.create();
+  hykkt_report_t r{};
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  r.be_4x4 = r.rr_4x4 = r.be_2x2 = r.rr_2x2 = r.be_2x2_scaled = r.rr_2x2_scaled = nan;
+  r.failed_column = -1;
+  r.symbolic_reused = 0;
+  // density_report (metrics.cpp:242-255) on the reduced pattern.
+  {
+    const idx hdiag = k.nx;  // H_tilde always stores the full diagonal
+    const idx hfull = 2 * (k.ht.nnz() - hdiag) + hdiag;
+    r.nnz_op = hfull + 2 * k.j.nnz() + k.nx;
+    r.nnz_fac = 2 * c.sp.l_nnz();
+    r.density_ratio = r.nnz_op > 0 ? static_cast<double>(r.nnz_fac) / r.nnz_op : 0.0;
+    r.rho_c = k.nx > 0 ? static_cast<double>(r.nnz_fac) / k.nx : 0.0;
+  }
+
+  ev.rec(0, st);
+  // ---- assembly: reduce, Ruiz, scale, H_gamma -------------------------
+  const long long nred = std::max<long long>(ap.n_ht, ap.nx);
+  dev::k_reduce<<<blocks_for(nred), kThreads, 0, st>>>(ap, c.hval.p, c.jdval.p, c.d_x.p, c.d_s.p,
+                                                       c.r_tx.p, c.r_s.p, c.r_yd.p, c.ht.p, c.r_x.p);
+  check_launch(c);
+  c.ruiz_flags.alloc(cfg.ruiz_max_iters + 2);
+  CK(cudaMemsetAsync(c.ruiz_flags.p, 0, sizeof(int) * (cfg.ruiz_max_iters + 2), st));
+  CK(cudaMemsetAsync(&c.status.p->abort, 0, sizeof(int), st));
+  {
+    dev::RuizArgs ra;
+    ra.p = ap;
+    ra.ht = c.ht.p;
+    ra.jval = c.jval.p;
+    ra.d = c.dscale.p;
+    ra.norms = c.norms.p;
+    ra.unconverged = c.ruiz_flags.p;
+    ra.sweeps_out = &c.status.p->ruiz_sweeps;
+    ra.max_iters = static_cast<int>(cfg.ruiz_max_iters);
+    ra.tol = cfg.ruiz_tol;
+    ra.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+    ra.abort = &c.status.p->abort;
+    coop_launch(c, (const void*)dev::k_ruiz, c.coop_ruiz_blocks, &ra);
+  }
+  const long long nsc = std::max<long long>({(long long)ap.n_ht, (long long)ap.nnz_j, (long long)ap.nx, (long long)ap.mc});
+  dev::k_scale<<<blocks_for(nsc), kThreads, 0, st>>>(ap, c.dscale.p, c.ht.p, c.jval.p, c.r_x.p, c.r_y.p,
+                                                     c.hts.p, c.js.p, c.js_csr.p, c.rxs.p, c.rys.p);
+  check_launch(c);
+  CK(cudaMemsetAsync(c.maxdiag.p, 0, sizeof(double), st));
+  const long long nhg = std::max<long long>(ap.n_hg, ap.nx);
+  dev::k_hgamma<<<blocks_for(nhg), kThreads, 0, st>>>(ap, cfg.gamma, c.hts.p, c.js.p, c.rxs.p, c.rys.p,
+                                                      c.hg.p, c.rhat.p, c.maxdiag.p);
+  check_launch(c);
+  ev.rec(1, st);
+
+  // ---- delta1 ladder (solver.cpp:108-142) --------------------------------
+  double dmin = (dmin_inout && *dmin_inout > 0.0) ? *dmin_inout : cfg.delta_min;
+  double delta1 = 0.0;
+  int attempts = 0;
+  auto attempt = [&](double d1) {
+    ++attempts;
+    return factor_attempt(c, c.hg.p, d1, 0.0, c.maxdiag.p, cfg.pivot_floor);
+  };
+  int failed = attempt(0.0);
+  while (failed >= 0 && delta1 <= cfg.delta_max / 2.0) {
+    if (delta1 == 0.0) {
+      delta1 = dmin;
+    } else {
+      dmin *= 2.0;
+      delta1 = dmin;
+    }
+    failed = attempt(delta1);
+  }
+  if (dmin_inout) *dmin_inout = dmin;
+  r.factorization_attempts = attempts;
+  r.delta1_final = delta1;
+  {
+    StatusBlock sb;
+    CK(cudaMemcpy(&sb, c.status.p, sizeof(sb), cudaMemcpyDeviceToHost));
+    r.ruiz_iterations = sb.ruiz_sweeps;
+  }
+  ev.rec(2, st);
+  if (failed >= 0) {
+    r.status = 2;  // kFailedDeltaMaxExceeded
+    r.failed_column = failed;
+    c.have_factor = false;
+    if (rep) *rep = r;
+    c.timing = hykkt_timing_t{};
+    c.timing.kernel_launches = c.launches - launches0;
+    return;
+  }
+  c.have_factor = true;
+
+  // ---- w = H^-1 r_hat_x, Schur rhs = J w - r_y ----------------------------
+  run_trsv(c, c.rhat.p, nullptr, c.js.p, nullptr);
+  if (k.mc > 0) {
+    dev::k_schur_rhs<<<blocks_for(k.mc), kThreads, 0, st>>>(static_cast<int>(k.mc), c.jcsr_rp.p, c.jcsr_ci_perm.p,
+                                                           c.js_csr.p, c.y.p, c.rys.p, c.cg_rhs.p);
+    check_launch(c);
+  }
+  ev.rec(3, st);
+
+  // ---- CG with the delta2 restart (solver.cpp:257-264) --------------------
+  const long long cg0 = c.launches;
+  dev::CgResultDev cg = run_cg(c, cfg, 0.0);
+  double delta2_used = 0.0;
+  if (cg.small_quadratic) {
+    cg = run_cg(c, cfg, cfg.delta2);
+    delta2_used = cfg.delta2;
+  }
+  const long long cg_launches = c.launches - cg0;
+  r.delta2_used = delta2_used;
+  r.cg_iterations = cg.iterations;
+  r.cg_relative_residual = cg.relres;
+  ev.rec(4, st);
+  if (!cg.converged) {
+    r.status = 3;  // kFailedCgNoConvergence
+    if (rep) *rep = r;
+    c.timing = hykkt_timing_t{};
+    c.timing.kernel_launches = c.launches - launches0;
+    c.timing.cg_kernel_launches = cg_launches;
+    return;
+  }
+  r.status = delta2_used > 0.0 ? 1 : 0;
+
+  // ---- dx = H^-1 (r_hat_x - J^T dy); unscale; recover ---------------------
+  run_trsv(c, c.rhat.p, c.cg_x.p, c.js.p, c.dx_s.p);
+  {
+    const long long nrec = std::max<long long>({(long long)k.nx, (long long)k.mc, (long long)k.md});
+    dev::k_recover<<<blocks_for(nrec), kThreads, 0, st>>>(ap, c.jdcsr_rp.p, c.jdcsr_ci.p, c.jdcsr_src.p, c.dscale.p,
+                                                          c.dx_s.p, c.cg_x.p, c.jdval.p, c.d_s.p, c.r_s.p, c.r_yd.p,
+                                                          c.dx.p, c.dy.p, c.ds.p, c.dyd.p);
+    check_launch(c);
+  }
+  ev.rec(5, st);
+  CK(cudaStreamSynchronize(st));
+  {
+    StatusBlock sb;
+    CK(cudaMemcpy(&sb, c.status.p, sizeof(sb), cudaMemcpyDeviceToHost));
+    if (sb.abort) throw TimeoutError("device wait timed out in the dx solve");
+  }
+  c.timing = hykkt_timing_t{};
+  if (ev.on) {
+    float ms[5];
+    for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev.e[i], ev.e[i + 1]));
+    c.timing.assemble_ms = ms[0];
+    c.timing.factor_ms = ms[1];
+    c.timing.solve_w_ms = ms[2];
+    c.timing.cg_ms = ms[3];
+    c.timing.solve_dx_ms = ms[4];
+    float tot;
+    CK(cudaEventElapsedTime(&tot, ev.e[0], ev.e[5]));
+    c.timing.total_ms = tot;
+  }
+  c.timing.kernel_launches = c.launches - launches0;
+  c.timing.cg_kernel_launches = cg_launches;
+
+  if (flags & HYKKT_FLAG_METRICS) {
+    const idx nx = k.nx, mc = k.mc, md = k.md;
+    auto dl = [&](const hykkt::DBuf<double>& b, idx n) {
+      std::vector<double> h(n);
+      if (n) CK(cudaMemcpy(h.data(), b.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+      return h;
+    };
+    const auto hv = dl(c.hval, k.h.nnz()), jv = dl(c.jval, k.j.nnz()), jdv = dl(c.jdval, k.jd.nnz());
+    const auto dxv = dl(c.d_x, nx), dsv = dl(c.d_s, md), rtx = dl(c.r_tx, nx), rs = dl(c.r_s, md),
+               ry = dl(c.r_y, mc), ryd = dl(c.r_yd, md);
+    const auto htv = dl(c.ht, k.ht.nnz()), htsv = dl(c.hts, k.ht.nnz()), jsv = dl(c.js, k.j.nnz());
+    const auto rx = dl(c.r_x, nx), rxs = dl(c.rxs, nx), rys = dl(c.rys, mc);
+    const auto sdx = dl(c.dx_s, nx), sdy = dl(c.cg_x, mc);
+    const auto odx = dl(c.dx, nx), ody = dl(c.dy, mc), ods = dl(c.ds, md), odyd = dl(c.dyd, md);
+    const CscView H{nx, nx, k.h.cp.data(), k.h.ri.data(), hv.data()};
+    const CscView J{mc, nx, k.j.cp.data(), k.j.ri.data(), jv.data()};
+    const CscView JD{md, nx, k.jd.cp.data(), k.jd.ri.data(), jdv.data()};
+    const CscView HT{nx, nx, k.ht.cp.data(), k.ht.ri.data(), htv.data()};
+    const CscView HTS{nx, nx, k.ht.cp.data(), k.ht.ri.data(), htsv.data()};
+    const CscView JS{mc, nx, k.j.cp.data(), k.j.ri.data(), jsv.data()};
+    const ErrorReport e2s = error_report_2x2(HTS, JS, rxs.data(), rys.data(), sdx.data(), sdy.data());
+    const ErrorReport e2 = error_report_2x2(HT, J, rx.data(), ry.data(), odx.data(), ody.data());
+    const ErrorReport e4 = error_report_4x4(H, J, JD, dxv.data(), dsv.data(), rtx.data(), rs.data(), ry.data(),
+                                            ryd.data(), odx.data(), ods.data(), ody.data(), odyd.data());
+    r.be_2x2_scaled = e2s.be;
+    r.rr_2x2_scaled = e2s.rr;
+    r.be_2x2 = e2.be;
+    r.rr_2x2 = e2.rr;
+    r.be_4x4 = e4.be;
+    r.rr_4x4 = e4.rr;
+  }
+  if (rep) *rep = r;
+}
+
+void download_solution(Ctx& c, double* dx, double* ds, double* dy, double* dyd) {
+  const KktPlan& k = c.kp;
+  auto dl = [&](const hykkt::DBuf<double>& b, double* out, idx n) {
+    if (out && n) CK(cudaMemcpyAsync(out, b.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  };
+  dl(c.dx, dx, k.nx);
+  dl(c.ds, ds, k.md);
+  dl(c.dy, dy, k.mc);
+  dl(c.dyd, dyd, k.md);
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HYKKT_OK;
+  } catch (const InvalidArgument& e) {
+    g_last_error = e.what();
+    return HYKKT_ERR_INVALID;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return HYKKT_ERR_CUDA;
+  } catch (const StateError& e) {
+    g_last_error = e.what();
+    return HYKKT_ERR_STATE;
+  } catch (const TimeoutError& e) {
+    g_last_error = e.what();
+    return HYKKT_ERR_DEVICE_TIMEOUT;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return HYKKT_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HYKKT_ERR_INVALID;
+  }
+}
+
+Ctx& ctx(hykkt_t h) {
+  if (!h) throw InvalidArgument("null handle");
+  CK(cudaSetDevice(h->device));
+  return *h;
+}
+
+}  // namespace
+}  // namespace hykkt
+
+using namespace hykkt;
+
+extern "C" {
+
+void hykkt_config_default(hykkt_config_t* cfg) {
+  if (!cfg) return;
+  cfg->gamma = 1e4;
+  cfg->delta_min = 1e-9;
+  cfg->delta_max = 1e-6;
+  cfg->delta2 = 1e-9;
+  cfg->cg_tol = 1e-12;
+  cfg->cg_max_iter = 500;
+  cfg->small_quadratic_threshold = 1e-12;
+  cfg->pivot_floor = 1e-13;
+  cfg->ruiz_tol = 0.01;
+  cfg->ruiz_max_iters = 20;
+}
+
+const char* hykkt_last_error(void) { return g_last_error.c_str(); }
+
+int hykkt_create(int device, hykkt_t* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("null output handle");
+    auto c = std::make_unique<hykkt_context>();
+    init_ctx(*c, device);
+    *out = c.release();
+  });
+}
+
+void hykkt_destroy(hykkt_t h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) {
+    cudaStreamSynchronize(h->stream);
+    cudaStreamDestroy(h->stream);
+  }
+  delete h;
+}
+
+int hykkt_analyze(hykkt_t h, int64_t n_x, int64_t m_c, int64_t m_d, const int64_t* h_colptr,
+                  const int64_t* h_rowidx, const int64_t* j_colptr, const int64_t* j_rowidx,
+                  const int64_t* jd_colptr, const int64_t* jd_rowidx, const int64_t* perm) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    analyze_kkt(c, n_x, m_c, m_d, h_colptr, h_rowidx, j_colptr, j_rowidx, jd_colptr, jd_rowidx, perm);
+  });
+}
+
+int hykkt_analysis_info(hykkt_t h, hykkt_analysis_t* out) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_plan) throw StateError("no analysis");
+    if (!out) throw InvalidArgument("null output");
+    const SupernodalPlan& s = c.sp;
+    hykkt_analysis_t a{};
+    a.n = s.n;
+    a.nnz_h_tilde = c.have_kkt ? c.kp.ht.nnz() : 0;
+    a.nnz_h_gamma = c.have_kkt ? c.kp.hg.nnz() : 0;
+    a.nnz_l = s.l_nnz();
+    a.n_supernodes = s.nsup;
+    a.n_levels = s.nlevels;
+    idx height = 0;
+    std::vector<idx> depth(s.n, 0);
+    for (idx j = s.n - 1; j >= 0; --j) {
+      depth[j] = s.parent[j] < 0 ? 1 : depth[s.parent[j]] + 1;
+      height = std::max(height, depth[j]);
+    }
+    a.etree_height = height;
+    a.max_sn_width = s.max_width;
+    a.max_sn_rows = s.max_nrows;
+    a.panel_slots = s.panel_size;
+    a.factor_flops = s.factor_flops;
+    a.nnz_j = c.have_kkt ? c.kp.j.nnz() : 0;
+    a.nnz_jd = c.have_kkt ? c.kp.jd.nnz() : 0;
+    a.m_c = c.have_kkt ? c.kp.mc : 0;
+    a.m_d = c.have_kkt ? c.kp.md : 0;
+    *out = a;
+  });
+}
+
+int hykkt_get_perm(hykkt_t h, int64_t* perm) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_plan) throw StateError("no analysis");
+    if (!perm) throw InvalidArgument("null output");
+    std::copy(c.sp.perm.begin(), c.sp.perm.end(), perm);
+  });
+}
+
+int hykkt_upload_values(hykkt_t h, const hykkt_values_t* values) {
+  return guarded([&] { upload_values(ctx(h), values); });
+}
+
+int hykkt_solve_resident(hykkt_t h, const hykkt_config_t* cfg, double* delta_min_inout, int flags,
+                         hykkt_report_t* report) {
+  return guarded([&] {
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    solve_resident(ctx(h), cfg ? *cfg : d, delta_min_inout, flags, report);
+  });
+}
+
+int hykkt_download_solution(hykkt_t h, double* dx, double* ds, double* dy, double* dyd) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_kkt) throw StateError("no analysis");
+    download_solution(c, dx, ds, dy, dyd);
+  });
+}
+
+int hykkt_solve_full(hykkt_t h, const hykkt_config_t* cfg, const hykkt_values_t* values,
+                     double* delta_min_inout, int flags, hykkt_report_t* report, double* dx, double* ds,
+                     double* dy, double* dyd) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    upload_values(c, values);
+    hykkt_report_t r{};
+    solve_resident(c, cfg ? *cfg : d, delta_min_inout, flags, &r);
+    if (r.status <= 1) download_solution(c, dx, ds, dy, dyd);
+    if (report) *report = r;
+  });
+}
+
+int hykkt_last_timing(hykkt_t h, hykkt_timing_t* out) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!out) throw InvalidArgument("null output");
+    *out = c.timing;
+  });
+}
+
+// ---- Cholesky-level hooks ---------------------------------------------------
+int hykkt_chol_analyze(hykkt_t h, int64_t n, const int64_t* colptr, const int64_t* rowidx,
+                       const int64_t* perm) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (n < 0) throw InvalidArgument("negative dimension");
+    CscPattern a = pattern_from(n, n, colptr, rowidx);
+    std::vector<idx> pv;
+    if (perm) pv.assign(perm, perm + n);
+    c.have_kkt = false;
+    c.kp = KktPlan{};
+    c.kp.hg = a;  // source pattern for scatter bookkeeping
+    c.sp = build_supernodal_plan(a, std::move(pv));
+    upload_plan(c, a);
+    c.src_vals.alloc(a.nnz());
+    CK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int hykkt_chol_factor(hykkt_t h, const double* values, double pivot_floor, int64_t* failed_column,
+                      double* failed_pivot) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_plan) throw StateError("hykkt_chol_analyze must be called first");
+    const idx nnz = static_cast<idx>(c.sp.src_to_panel.size());
+    if (nnz > 0 && !values) throw InvalidArgument("null values");
+    if (c.src_vals.n < static_cast<std::size_t>(nnz)) c.src_vals.alloc(nnz);
+    if (nnz) CK(cudaMemcpyAsync(c.src_vals.p, values, nnz * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    const int fc = factor_attempt(c, c.src_vals.p, 0.0, pivot_floor, nullptr, 0.0);
+    if (failed_column) *failed_column = fc;
+    if (fc >= 0) {
+      double piv = 0.0;
+      CK(cudaMemcpy(&piv, c.panel.p + c.sp.diag_panel[fc], sizeof(double), cudaMemcpyDeviceToHost));
+      if (failed_pivot) *failed_pivot = piv;
+      c.have_factor = false;
+    } else {
+      if (failed_pivot) *failed_pivot = 0.0;
+      c.have_factor = true;
+    }
+  });
+}
+
+int hykkt_chol_solve(hykkt_t h, const double* b, double* x) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_factor) throw StateError("no successful factorization");
+    const idx n = c.sp.n;
+    if (n == 0) return;
+    if (!b || !x) throw InvalidArgument("null vector");
+    CK(cudaMemcpyAsync(c.bvec.p, b, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaMemsetAsync(&c.status.p->abort, 0, sizeof(int), c.stream));
+    run_trsv(c, c.bvec.p, nullptr, nullptr, c.xvec.p);
+    CK(cudaMemcpyAsync(x, c.xvec.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    read_status(c);
+  });
+}
+
+int hykkt_chol_get_factor(hykkt_t h, int64_t* l_colptr, int64_t* l_rowidx, double* l_values,
+                          int64_t* parent) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_plan) throw StateError("no analysis");
+    const SupernodalPlan& s = c.sp;
+    if (l_colptr) std::copy(s.l_cp.begin(), s.l_cp.end(), l_colptr);
+    if (l_rowidx) std::copy(s.l_ri.begin(), s.l_ri.end(), l_rowidx);
+    if (parent) std::copy(s.parent.begin(), s.parent.end(), parent);
+    if (l_values) {
+      if (!c.have_factor) throw StateError("no successful factorization");
+      std::vector<double> pan(s.panel_size);
+      if (s.panel_size) CK(cudaMemcpy(pan.data(), c.panel.p, s.panel_size * sizeof(double), cudaMemcpyDeviceToHost));
+      for (std::size_t q = 0; q < s.l_to_panel.size(); ++q) l_values[q] = pan[s.l_to_panel[q]];
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,318 @@
+"""Host-side mirror of the reference solver API over the B200 C ABI.
+
+Names, argument meaning, defaults and outcomes follow
+/root/reference/proj/core/include/hkkt/solver.hpp and cholesky.hpp:
+
+  SolverConfig / RegularizationState / SolveStatus / SolveReport   solver.hpp:29-150
+  solve_full / solve_sequence / SequenceResult                     solver.hpp:172-205
+  symbolic_cholesky / numeric_cholesky / factor_solve              cholesky.hpp:41-83
+  NotSpdFailure                                                    cholesky.hpp:47-50
+
+Every numeric step runs in libhykkt.so on the GPU; there is no CPU fallback
+(a missing library or a CUDA failure raises).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field, fields
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dp, f64, i64, ip
+from .kkt import BlockKkt4x4, CscMatrix, FullSolution
+
+
+@dataclass
+class SolverConfig:
+    gamma: float = 1e4
+    delta_min: float = 1e-9
+    delta_max: float = 1e-6
+    delta2: float = 1e-9
+    cg_tol: float = 1e-12
+    cg_max_iter: int = 500
+    small_quadratic_threshold: float = 1e-12
+    pivot_floor: float = 1e-13
+    ruiz_tol: float = 0.01
+    ruiz_max_iters: int = 20
+
+    def c(self) -> _lib.Config:
+        return _lib.Config(*[getattr(self, f.name) for f in fields(self)])
+
+
+class SolveStatus(enum.IntEnum):
+    kSolved = 0
+    kSolvedWithDelta2 = 1
+    kFailedDeltaMaxExceeded = 2
+    kFailedCgNoConvergence = 3
+
+
+def is_success(s) -> bool:
+    return SolveStatus(s) in (SolveStatus.kSolved, SolveStatus.kSolvedWithDelta2)
+
+
+@dataclass
+class RegularizationState:
+    delta1: float = 0.0
+    delta_min_current: float = 0.0
+    attempts: int = 0
+
+    @staticmethod
+    def initial(cfg: SolverConfig) -> "RegularizationState":
+        return RegularizationState(0.0, cfg.delta_min, 0)
+
+
+@dataclass
+class SolveReport:
+    status: SolveStatus = SolveStatus.kSolved
+    delta1_final: float = 0.0
+    delta2_used: float = 0.0
+    cg_iterations: int = 0
+    factorization_attempts: int = 0
+    be_4x4: float = 0.0
+    rr_4x4: float = 0.0
+    be_2x2: float = 0.0
+    rr_2x2: float = 0.0
+    be_2x2_scaled: float = 0.0
+    rr_2x2_scaled: float = 0.0
+    symbolic_reused: bool = False
+    nnz_op: int = 0
+    nnz_fac: int = 0
+    density_ratio: float = 0.0
+    rho_c: float = 0.0
+    ruiz_iterations: int = 0
+    cg_relative_residual: float = 0.0
+    failure_detail: str = ""
+
+    @staticmethod
+    def from_c(r: _lib.Report) -> "SolveReport":
+        rep = SolveReport(
+            status=SolveStatus(r.status), delta1_final=r.delta1_final, delta2_used=r.delta2_used,
+            cg_iterations=r.cg_iterations, factorization_attempts=r.factorization_attempts,
+            be_4x4=r.be_4x4, rr_4x4=r.rr_4x4, be_2x2=r.be_2x2, rr_2x2=r.rr_2x2,
+            be_2x2_scaled=r.be_2x2_scaled, rr_2x2_scaled=r.rr_2x2_scaled,
+            symbolic_reused=bool(r.symbolic_reused), nnz_op=r.nnz_op, nnz_fac=r.nnz_fac,
+            density_ratio=r.density_ratio, rho_c=r.rho_c, ruiz_iterations=r.ruiz_iterations,
+            cg_relative_residual=r.cg_relative_residual)
+        if rep.status == SolveStatus.kFailedDeltaMaxExceeded:
+            rep.failure_detail = (f"factorization failed up to delta1 = {rep.delta1_final:f} "
+                                  f"at column {r.failed_column}")
+        elif rep.status == SolveStatus.kFailedCgNoConvergence:
+            rep.failure_detail = f"CG stalled at relative residual {rep.cg_relative_residual:f}"
+        return rep
+
+
+@dataclass
+class FullSolveResult:
+    solution: Optional[FullSolution]
+    report: SolveReport
+    symbolic_created: bool = False
+
+
+@dataclass
+class SequenceStats:
+    symbolic_analyses: int = 0
+    numeric_factorizations: int = 0
+    factorization_attempts: int = 0
+
+
+@dataclass
+class SequenceResult:
+    reports: list = field(default_factory=list)
+    solutions: list = field(default_factory=list)
+    stats: SequenceStats = field(default_factory=SequenceStats)
+    pattern_uniform: bool = True
+
+    def all_successful(self) -> bool:
+        return all(is_success(r.status) for r in self.reports)
+
+
+@dataclass
+class NotSpdFailure:
+    column: int
+    pivot: float
+
+
+class Device:
+    """One libhykkt handle: a device, a stream and one analysed pattern."""
+
+    def __init__(self, device: int = 0):
+        L = _lib.lib()
+        h = C.c_void_p()
+        check(L.hykkt_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self._pattern = None  # the BlockKkt4x4 whose pattern was analysed
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().hykkt_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- analysis ----------------------------------------------------------
+    def analyze(self, sys: BlockKkt4x4, perm=None) -> None:
+        """Per-pattern half of solve_reduced (solver.cpp:230-235), once."""
+        L = _lib.lib()
+        a = [i64(x) for x in (sys.h.colptr, sys.h.rowidx, sys.j.colptr, sys.j.rowidx,
+                              sys.j_d.colptr, sys.j_d.rowidx)]
+        p = None if perm is None else i64(perm)
+        check(L.hykkt_analyze(self.h, sys.n_x, sys.m_c, sys.m_d, *[ip(x) for x in a], ip(p)))
+        self._pattern = sys
+
+    def info(self) -> dict:
+        a = _lib.Analysis()
+        check(_lib.lib().hykkt_analysis_info(self.h, C.byref(a)))
+        return {n: getattr(a, n) for n, _ in a._fields_}
+
+    def perm(self) -> np.ndarray:
+        n = self.info()["n"]
+        out = np.zeros(n, np.int64)
+        check(_lib.lib().hykkt_get_perm(self.h, ip(out)))
+        return out
+
+    # ---- values ------------------------------------------------------------
+    def _values(self, sys: BlockKkt4x4):
+        arrs = [f64(x) for x in (sys.h.values, sys.j.values, sys.j_d.values, sys.d_x, sys.d_s,
+                                 sys.r_tilde_x, sys.r_s, sys.r_y, sys.r_yd)]
+        self._keep = arrs
+        return _lib.Values(*[dp(x) for x in arrs])
+
+    def upload(self, sys: BlockKkt4x4) -> None:
+        v = self._values(sys)
+        check(_lib.lib().hykkt_upload_values(self.h, C.byref(v)))
+
+    def solve_resident(self, cfg: SolverConfig, state: RegularizationState | None = None,
+                       metrics: bool = False, timing: bool = False) -> SolveReport:
+        rep = _lib.Report()
+        dm = C.c_double(state.delta_min_current if state else 0.0)
+        flags = (_lib.FLAG_METRICS if metrics else 0) | (_lib.FLAG_TIMING if timing else 0)
+        check(_lib.lib().hykkt_solve_resident(self.h, C.byref(cfg.c()), C.byref(dm), flags,
+                                              C.byref(rep)))
+        if state is not None:
+            state.delta_min_current = dm.value
+            state.delta1 = rep.delta1_final
+            state.attempts = rep.factorization_attempts
+        return SolveReport.from_c(rep)
+
+    def download(self) -> FullSolution:
+        s = self._pattern
+        out = FullSolution(np.zeros(s.n_x), np.zeros(s.m_d), np.zeros(s.m_c), np.zeros(s.m_d))
+        check(_lib.lib().hykkt_download_solution(self.h, dp(out.dx), dp(out.ds), dp(out.dy),
+                                                 dp(out.dyd)))
+        return out
+
+    def timing(self) -> dict:
+        t = _lib.Timing()
+        check(_lib.lib().hykkt_last_timing(self.h, C.byref(t)))
+        return {n: getattr(t, n) for n, _ in t._fields_}
+
+    def solve_full(self, sys: BlockKkt4x4, cfg: SolverConfig | None = None,
+                   state: RegularizationState | None = None,
+                   metrics: bool = True) -> FullSolveResult:
+        """hkkt::solve_full (solver.cpp:295-328) with this handle's symbolic
+        analysis (analysed on first use, like a null `shared`)."""
+        cfg = cfg or SolverConfig()
+        created = False
+        if self._pattern is None or not self._pattern.same_pattern_as(sys):
+            self.analyze(sys)
+            created = True
+        if state is None:
+            state = RegularizationState.initial(cfg)
+        v = self._values(sys)
+        rep = _lib.Report()
+        dm = C.c_double(state.delta_min_current)
+        sol = FullSolution(np.zeros(sys.n_x), np.zeros(sys.m_d), np.zeros(sys.m_c),
+                           np.zeros(sys.m_d))
+        flags = _lib.FLAG_METRICS if metrics else 0
+        check(_lib.lib().hykkt_solve_full(self.h, C.byref(cfg.c()), C.byref(v), C.byref(dm),
+                                          flags, C.byref(rep), dp(sol.dx), dp(sol.ds),
+                                          dp(sol.dy), dp(sol.dyd)))
+        state.delta_min_current = dm.value
+        state.delta1 = rep.delta1_final
+        state.attempts = rep.factorization_attempts
+        report = SolveReport.from_c(rep)
+        return FullSolveResult(sol if is_success(report.status) else None, report, created)
+
+
+def solve_full(sys: BlockKkt4x4, cfg: SolverConfig | None = None, shared: Device | None = None,
+               state: RegularizationState | None = None) -> FullSolveResult:
+    dev = shared or Device()
+    return dev.solve_full(sys, cfg, state)
+
+
+def solve_sequence(systems: Sequence[BlockKkt4x4], cfg: SolverConfig | None = None,
+                   device: int = 0) -> SequenceResult:
+    """hkkt::solve_sequence (solver.cpp:352-412): one symbolic analysis when
+    the patterns are uniform, delta_min carried across, failures recorded
+    and the sequence continued."""
+    if len(systems) == 0:
+        raise _lib.InvalidMatrixError(-1, "solve_sequence: empty sequence")
+    cfg = cfg or SolverConfig()
+    res = SequenceResult()
+    res.pattern_uniform = all(s.same_pattern_as(systems[0]) for s in systems[1:])
+    dev = Device(device)
+    state = RegularizationState.initial(cfg)
+    for k, sys in enumerate(systems):
+        if not res.pattern_uniform:
+            dev._pattern = None
+        r = dev.solve_full(sys, cfg, state)
+        r.report.symbolic_reused = res.pattern_uniform and k > 0
+        if r.symbolic_created:
+            res.stats.symbolic_analyses += 1
+        res.stats.factorization_attempts += r.report.factorization_attempts
+        if r.report.status != SolveStatus.kFailedDeltaMaxExceeded:
+            res.stats.numeric_factorizations += 1
+        res.reports.append(r.report)
+        res.solutions.append(r.solution)
+    dev.close()
+    return res
+
+
+class CholeskyFactor:
+    """symbolic_cholesky + numeric_cholesky + factor_solve on the device
+    (cholesky.hpp:41-83) for a general SPD matrix in lower CSC storage."""
+
+    def __init__(self, a_lower: CscMatrix, perm=None, device: int = 0):
+        self.dev = Device(device)
+        self.n = a_lower.ncols
+        self._cp, self._ri = i64(a_lower.colptr), i64(a_lower.rowidx)
+        p = None if perm is None else i64(perm)
+        check(_lib.lib().hykkt_chol_analyze(self.dev.h, self.n, ip(self._cp), ip(self._ri), ip(p)))
+        self.ok = False
+
+    def factorize(self, values, pivot_floor: float = 0.0):
+        """Returns None on success or NotSpdFailure (a value, as in the
+        reference)."""
+        v = f64(values)
+        fc, fp = C.c_int64(0), C.c_double(0)
+        check(_lib.lib().hykkt_chol_factor(self.dev.h, dp(v), pivot_floor, C.byref(fc),
+                                           C.byref(fp)))
+        self.ok = fc.value < 0
+        return None if self.ok else NotSpdFailure(int(fc.value), float(fp.value))
+
+    def solve(self, b) -> np.ndarray:
+        b = f64(b)
+        if b.shape[0] != self.n:
+            raise _lib.InvalidMatrixError(-1, f"factor_solve: rhs has length {b.shape[0]}, "
+                                              f"expected {self.n}")
+        x = np.zeros(self.n)
+        check(_lib.lib().hykkt_chol_solve(self.dev.h, dp(b), dp(x)))
+        return x
+
+    def factor(self) -> dict:
+        info = self.dev.info()
+        n, nnz = info["n"], info["nnz_l"]
+        cp, ri, par = np.zeros(n + 1, np.int64), np.zeros(nnz, np.int64), np.zeros(n, np.int64)
+        lv = np.zeros(nnz) if self.ok else None
+        check(_lib.lib().hykkt_chol_get_factor(self.dev.h, ip(cp), ip(ri), dp(lv), ip(par)))
+        return dict(l_colptr=cp, l_rowidx=ri, l_values=lv, parent=par, perm=self.dev.perm())
