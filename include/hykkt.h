@@ -140,6 +140,15 @@ int hykkt_analyze(hykkt_t h, int64_t n_x, int64_t m_c, int64_t m_d,
                   const int64_t* jd_colptr, const int64_t* jd_rowidx,
                   const int64_t* perm);
 int hykkt_analysis_info(hykkt_t h, hykkt_analysis_t* out);
+/* Host-only analysis (no device needed): the same ordering + symbolic +
+ * supernode plan hykkt_analyze builds, returning its statistics and the
+ * ordering used (perm_out may be NULL). */
+int hykkt_host_analyze(int64_t n_x, int64_t m_c, int64_t m_d,
+                       const int64_t* h_colptr, const int64_t* h_rowidx,
+                       const int64_t* j_colptr, const int64_t* j_rowidx,
+                       const int64_t* jd_colptr, const int64_t* jd_rowidx,
+                       const int64_t* perm, int64_t* perm_out,
+                       hykkt_analysis_t* out);
 int hykkt_get_perm(hykkt_t h, int64_t* perm /* n */);
 
 /* solve_full (solver.cpp:295-328) on one system: values and outputs are

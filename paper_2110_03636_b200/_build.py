@@ -17,7 +17,7 @@ CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CPP_SOURCES = ["analyze.cpp", "host_metrics.cpp"]
-CU_SOURCES = ["hykkt_cuda.cu", "hykkt_batch.cu"]
+CU_SOURCES = ["hykkt_cuda.cu"]
 HEADERS = list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + [INCLUDE / "hykkt.h"]
 
 

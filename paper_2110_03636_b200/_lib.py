@@ -81,7 +81,7 @@ FLAG_TIMING = 2
 # Every symbol include/hykkt.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "hykkt_config_default", "hykkt_last_error", "hykkt_create", "hykkt_destroy",
-    "hykkt_analyze", "hykkt_analysis_info", "hykkt_get_perm", "hykkt_solve_full",
+    "hykkt_analyze", "hykkt_analysis_info", "hykkt_host_analyze", "hykkt_get_perm", "hykkt_solve_full",
     "hykkt_upload_values", "hykkt_solve_resident", "hykkt_download_solution",
     "hykkt_last_timing", "hykkt_chol_analyze", "hykkt_chol_factor", "hykkt_chol_solve",
     "hykkt_chol_get_factor", "hykkt_batch_solve", "hykkt_batch_upload",
@@ -124,6 +124,8 @@ def lib() -> C.CDLL:
                                 I64P, I64P, I64P]
     L.hykkt_analysis_info.argtypes = [vp, C.POINTER(Analysis)]
     L.hykkt_get_perm.argtypes = [vp, I64P]
+    L.hykkt_host_analyze.argtypes = [C.c_int64, C.c_int64, C.c_int64, I64P, I64P, I64P, I64P,
+                                     I64P, I64P, I64P, I64P, C.POINTER(Analysis)]
     L.hykkt_solve_full.argtypes = [vp, C.POINTER(Config), C.POINTER(Values), F64P, C.c_int,
                                    C.POINTER(Report), F64P, F64P, F64P, F64P]
     L.hykkt_upload_values.argtypes = [vp, C.POINTER(Values)]

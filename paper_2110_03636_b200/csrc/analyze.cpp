@@ -339,6 +339,7 @@ SupernodalPlan build_supernodal_plan(const CscPattern& a,
   }
   std::partial_sum(s.lrow_ptr.begin(), s.lrow_ptr.end(), s.lrow_ptr.begin());
   s.lrow_col.resize(s.lrow_ptr[n]);
+  s.lrow_row.resize(s.lrow_ptr[n]);
   s.lrow_pos.resize(s.lrow_ptr[n]);
   {
     std::vector<int> cur(s.lrow_ptr.begin(), s.lrow_ptr.end() - 1);
@@ -350,7 +351,59 @@ SupernodalPlan build_supernodal_plan(const CscPattern& a,
         for (int t = w; t < nr; ++t) {
           const int q = cur[rows[t]]++;
           s.lrow_col[q] = f + k;
+          s.lrow_row[q] = rows[t];
           s.lrow_pos[q] = static_cast<int>(s.sn_off[d] + idx{k} * nr + t);
+        }
+      }
+    }
+  }
+
+  // Update-vector storage and child -> parent extend-add gather maps.
+  s.u_off.assign(ns + 1, 0);
+  s.ext_ptr.assign(ns + 1, 0);
+  for (idx k = 0; k < ns; ++k) {
+    const int w = s.sn_first[k + 1] - s.sn_first[k];
+    s.u_off[k + 1] = s.u_off[k] + (s.sn_nrows[k] - w);
+    const int p = s.sn_parent[k];
+    s.ext_ptr[k + 1] = s.ext_ptr[k] + (p >= 0 ? s.sn_nrows[p] : 0);
+  }
+  s.ext_map.assign(s.ext_ptr[ns], -1);
+  s.relind.assign(s.u_off[ns], -1);
+  for (idx k = 0; k < ns; ++k) {
+    const int p = s.sn_parent[k];
+    if (p < 0) continue;
+    const int w = s.sn_first[k + 1] - s.sn_first[k];
+    const int* rc = s.sn_rows.data() + s.sn_rows_ptr[k];
+    const int* rp = s.sn_rows.data() + s.sn_rows_ptr[p];
+    const int nrp = s.sn_nrows[p];
+    int q = 0;
+    for (int t = w; t < s.sn_nrows[k]; ++t) {  // both lists ascending
+      while (q < nrp && rp[q] < rc[t]) ++q;
+      if (q == nrp || rp[q] != rc[t]) fail("internal: child row not in parent structure");
+      s.ext_map[s.ext_ptr[k] + q] = t - w;
+      s.relind[s.u_off[k] + t - w] = q;
+    }
+  }
+
+  {
+    const int nslot = s.sn_rows_ptr[ns];
+    s.gat_ptr.assign(nslot + 1, 0);
+    for (idx k = 0; k < ns; ++k) {
+      const int p = s.sn_parent[k];
+      if (p < 0) continue;
+      for (int q = 0; q < s.sn_nrows[p]; ++q) {
+        if (s.ext_map[s.ext_ptr[k] + q] >= 0) s.gat_ptr[s.sn_rows_ptr[p] + q + 1]++;
+      }
+    }
+    std::partial_sum(s.gat_ptr.begin(), s.gat_ptr.end(), s.gat_ptr.begin());
+    s.gat_idx.resize(s.gat_ptr[nslot]);
+    std::vector<int> cur(s.gat_ptr.begin(), s.gat_ptr.end() - 1);
+    for (idx p = 0; p < ns; ++p) {  // children in ascending order per parent
+      for (int c = s.child_ptr[p]; c < s.child_ptr[p + 1]; ++c) {
+        const int k = s.child[c];
+        for (int q = 0; q < s.sn_nrows[p]; ++q) {
+          const int t = s.ext_map[s.ext_ptr[k] + q];
+          if (t >= 0) s.gat_idx[cur[s.sn_rows_ptr[p] + q]++] = s.u_off[k] + t;
         }
       }
     }

@@ -70,8 +70,23 @@ struct SupernodalPlan {
 
   // forward-solve row lists: strictly-lower entries of L row i that lie in
   // earlier supernodes, as (column, panel slot), ascending column.
-  std::vector<int> lrow_ptr, lrow_col;
+  std::vector<int> lrow_ptr, lrow_col, lrow_row;
   std::vector<int> lrow_pos;
+
+  // multifrontal forward solve: supernode s passes an update vector u_s of
+  // length nrows - width (rows below its diagonal block) to its parent.
+  // u_off[s] = offset of u_s; for child c, ext_map[ext_ptr[c] + q] is the
+  // index in u_c of the parent's row-structure position q, or -1.
+  std::vector<int> u_off;      // nsup + 1
+  std::vector<int> ext_ptr;    // nsup + 1
+  std::vector<int> ext_map;
+  // flattened gather lists: for position q of supernode s (slot
+  // sn_rows_ptr[s] + q) the absolute u indices to sum, in child order.
+  std::vector<int> gat_ptr;    // sn_rows_ptr[nsup] + 1
+  std::vector<int> gat_idx;
+  // child-side form of the same map: relind[u_off[c] + t] = position in the
+  // parent's row structure of the child's update-vector entry t.
+  std::vector<int> relind;
 
   // L CSC position (reference layout) -> panel slot
   std::vector<int> l_to_panel;

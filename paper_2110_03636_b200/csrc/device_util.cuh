@@ -34,6 +34,26 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// acq_rel fence at gpu scope.  Cheaper than __threadfence() (fence.sc) and,
+// used once per task rather than per poll, keeps L1 invalidations (the
+// CCTL.IVALL an acquire at gpu scope implies) off the spin loops.
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Producer side of a task flag: every lane orders its own writes, the warp
+// converges, one lane publishes.
+__device__ __forceinline__ void warp_publish(int* flag, int value, int lane) {
+  fence_gpu();
+  __syncwarp();
+  if (lane == 0) st_relaxed(flag, value);
+}
 
 // Values produced by other SMs inside the same launch are read through L2
 // (ld.global.cg); L1 is not coherent across SMs.
@@ -41,21 +61,26 @@ __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ void stcg(double* p, double v) { __stcg(p, v); }
 
 // Waits until *flag == want. Returns false (and raises *abort) on timeout
-// or when another waiter already aborted.
+// or when another waiter already aborted.  The shared abort word and the
+// clock are only consulted every 256 polls: thousands of waiters polling one
+// word would serialise on a single L2 slice and slow every wake-up.
 __device__ __forceinline__ bool wait_flag(const int* flag, int want, int* abort) {
-  if (ld_acquire(flag) == want) return true;
-  const long long t0 = clock64();
-  unsigned ns = 20;
-  for (;;) {
-    if (ld_acquire(flag) == want) return true;
-    if (ld_relaxed(abort)) return false;
-    if (clock64() - t0 > kSpinBudget) {
-      atomicExch(abort, 1);
-      return false;
+  if (ld_relaxed(flag) != want) {
+    const long long t0 = clock64();
+    for (unsigned it = 1;; ++it) {
+      __nanosleep(20);
+      if (ld_relaxed(flag) == want) break;
+      if ((it & 255u) == 0u) {
+        if (ld_relaxed(abort)) return false;
+        if (clock64() - t0 > kSpinBudget) {
+          atomicExch(abort, 1);
+          return false;
+        }
+      }
     }
-    __nanosleep(ns);
-    if (ns < 200) ns += 20;
   }
+  fence_gpu();
+  return true;
 }
 
 struct GridBarrier {
@@ -67,24 +92,24 @@ struct GridBarrier {
 __device__ __forceinline__ void grid_sync(const GridBarrier& b, int* abort) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = ld_acquire(b.gen);
-    __threadfence();
+    const unsigned g = ld_relaxed(b.gen);
+    fence_gpu();
     const unsigned arrived = atomicAdd(b.count, 1u);
     if (arrived == gridDim.x - 1) {
       atomicExch(b.count, 0u);
-      __threadfence();
-      st_release(b.gen, g + 1);
+      fence_gpu();
+      atomicExch(b.gen, g + 1);
     } else {
       const long long t0 = clock64();
-      while (ld_acquire(b.gen) == g) {
-        if (ld_relaxed(abort) || clock64() - t0 > kSpinBudget) {
+      for (unsigned it = 1; ld_relaxed(b.gen) == g; ++it) {
+        if ((it & 255u) == 0u && (ld_relaxed(abort) || clock64() - t0 > kSpinBudget)) {
           atomicExch(abort, 1);
           break;
         }
-        __nanosleep(32);
+        __nanosleep(20);
       }
     }
-    __threadfence();
+    fence_gpu();
   }
   __syncthreads();
 }

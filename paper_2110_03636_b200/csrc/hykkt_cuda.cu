@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -107,10 +108,12 @@ struct hykkt_context {
 
   // device supernodal plan
   hykkt::DBuf<int> order, first, nrows, off, rows_ptr, rows, parent, child_ptr, child;
-  hykkt::DBuf<int> upd_ptr, upd_d, upd_off, upd_cnt, lrow_ptr, lrow_col, lrow_pos;
+  hykkt::DBuf<int> upd_ptr, upd_d, upd_off, upd_cnt, lrow_ptr, lrow_col, lrow_pos, lrow_row;
+  hykkt::DBuf<double> lrow_val, xsol, ubuf, accbuf;
+  hykkt::DBuf<int> u_off, ext_ptr, ext_map, gat_ptr, gat_idx, relind;
   hykkt::DBuf<int> perm, iperm, src_to_panel, src_row, src_col;
   hykkt::DBuf<double> panel, y, src_vals, bvec, xvec;
-  hykkt::DBuf<int> fdone, bdone, fac_done;
+  hykkt::DBuf<int> fac_done;
   hykkt::DBuf<unsigned> barrier;  // count, gen
   hykkt::DBuf<hykkt::StatusBlock> status;
   int epoch = 0;
@@ -130,6 +133,14 @@ struct hykkt_context {
 
   hykkt_timing_t timing{};
   long long launches = 0;
+
+  // Active value / output pointers: the single-system buffers above, or one
+  // slot of the resident batch below.
+  struct VPtr { double *h, *j, *jd, *dx, *ds, *rtx, *rs, *ry, *ryd; } v{};
+  struct OPtr { double *dx, *dy, *ds, *dyd; } o{};
+  hykkt::DBuf<double> bvals, bouts;  // [batch][values], [batch][solution]
+  long long batch = 0;
+  std::vector<hykkt_report_t> batch_reports;
 
   hykkt::dev::SnPlan snplan() const {
     hykkt::dev::SnPlan s;
@@ -153,6 +164,13 @@ struct hykkt_context {
     s.lrow_pos = lrow_pos.p;
     s.perm = perm.p;
     s.iperm = iperm.p;
+    s.u_off = u_off.p;
+    s.ext_ptr = ext_ptr.p;
+    s.ext_map = ext_map.p;
+    s.gat_ptr = gat_ptr.p;
+    s.gat_idx = gat_idx.p;
+    s.relind = relind.p;
+    s.u_size = sp.u_off.empty() ? 0 : sp.u_off.back();
     return s;
   }
 
@@ -204,10 +222,15 @@ void check_launch(Ctx& c) {
   c.launches++;
 }
 
+// Resident blocks for a cooperative persistent kernel: occupancy-limited and
+// capped at HYKKT_BLOCKS_PER_SM (default 4 -> 32 warps per SM): more
+// resident warps than that only add pollers.
 int occupancy_blocks(Ctx& c, const void* fn) {
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
-  return std::max(1, per_sm) * c.num_sms;
+  int cap = 4;
+  if (const char* e = std::getenv("HYKKT_BLOCKS_PER_SM")) cap = std::max(1, std::atoi(e));
+  return std::max(1, std::min(per_sm, cap)) * c.num_sms;
 }
 
 void init_ctx(Ctx& c, int device) {
@@ -247,6 +270,17 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   c.lrow_ptr.upload(s.lrow_ptr, st);
   c.lrow_col.upload(s.lrow_col, st);
   c.lrow_pos.upload(s.lrow_pos, st);
+  c.lrow_row.upload(s.lrow_row, st);
+  c.lrow_val.alloc(s.lrow_pos.size());
+  c.xsol.alloc(s.n);
+  c.u_off.upload(s.u_off, st);
+  c.ext_ptr.upload(s.ext_ptr, st);
+  c.ext_map.upload(s.ext_map, st);
+  c.gat_ptr.upload(s.gat_ptr, st);
+  c.gat_idx.upload(s.gat_idx, st);
+  c.relind.upload(s.relind, st);
+  c.ubuf.alloc(s.u_off.back());
+  c.accbuf.alloc(s.sn_rows_ptr.back());
   c.perm.upload(to_i32(s.perm), st);
   c.iperm.upload(to_i32(s.iperm), st);
   c.src_to_panel.upload(s.src_to_panel, st);
@@ -263,11 +297,7 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   c.y.alloc(s.n);
   c.bvec.alloc(s.n);
   c.xvec.alloc(s.n);
-  c.fdone.alloc(s.nsup);
-  c.bdone.alloc(s.nsup);
   c.fac_done.alloc(s.nsup);
-  CK(cudaMemsetAsync(c.fdone.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
-  CK(cudaMemsetAsync(c.bdone.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   c.epoch = 0;
   c.have_plan = true;
@@ -315,43 +345,47 @@ int factor_attempt(Ctx& c, const double* src, double delta1, double floor_abs,
   fa.abort = &c.status.p->abort;
   if (s.nsup > 0) coop_launch(c, (const void*)dev::k_factor, c.coop_factor_blocks, &fa);
   const StatusBlock sb = read_status(c);
-  return sb.fail_col >= static_cast<int>(s.n) ? -1 : sb.fail_col;
+  const int failed = sb.fail_col >= static_cast<int>(s.n) ? -1 : sb.fail_col;
+  return failed;
 }
 
-void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, double* x_out) {
-  const SupernodalPlan& s = c.sp;
-  if (s.nsup == 0) return;
+dev::TrsvArgs trsv_args(Ctx& c) {
   dev::TrsvArgs ta;
   ta.s = c.snplan();
   ta.panel = c.panel.p;
   ta.y = c.y.p;
-  ta.x_out = x_out;
-  ta.fdone = c.fdone.p;
-  ta.bdone = c.bdone.p;
-  ta.epoch = ++c.epoch;
+  ta.x = c.xsol.p;
+  ta.u = c.ubuf.p;
+  ta.acc_buf = c.accbuf.p;
+  ta.x_out = nullptr;
   ta.abort = &c.status.p->abort;
-  ta.rhs.b = b;
-  ta.rhs.u = u;
+  ta.rhs.b = nullptr;
+  ta.rhs.u = nullptr;
   ta.rhs.j_cp = c.j_cp.p;
   ta.rhs.j_ri = c.j_ri.p;
+  ta.rhs.jval = nullptr;
+  ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+  ta.trace = nullptr;
+  return ta;
+}
+
+// One H^-1 application; the result stays in c.xsol (permuted order) and,
+// when x_out is given, is scattered to original order there.
+void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, double* x_out) {
+  const SupernodalPlan& s = c.sp;
+  if (s.nsup == 0) return;
+  dev::TrsvArgs ta = trsv_args(c);
+  ta.x_out = x_out;
+  ta.rhs.b = b;
+  ta.rhs.u = u;
   ta.rhs.jval = jval;
   coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
 }
 
 dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   dev::CgArgs a;
-  a.tr.s = c.snplan();
-  a.tr.panel = c.panel.p;
-  a.tr.y = c.y.p;
-  a.tr.x_out = nullptr;
-  a.tr.fdone = c.fdone.p;
-  a.tr.bdone = c.bdone.p;
-  a.tr.epoch = 0;
-  a.tr.abort = &c.status.p->abort;
-  a.tr.rhs.b = nullptr;
+  a.tr = trsv_args(c);
   a.tr.rhs.u = c.cg_p.p;
-  a.tr.rhs.j_cp = c.j_cp.p;
-  a.tr.rhs.j_ri = c.j_ri.p;
   a.tr.rhs.jval = c.js.p;
   a.mc = static_cast<int>(c.kp.mc);
   a.jcsr_rp = c.jcsr_rp.p;
@@ -367,12 +401,9 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   a.tol = cfg.cg_tol;
   a.thr = cfg.small_quadratic_threshold;
   a.max_iter = cfg.cg_max_iter;
-  a.epoch_base = c.epoch;
   a.res = &c.status.p->cg;
-  a.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
   if (c.sp.nsup == 0 && c.kp.mc > 0) throw StateError("empty factor with constraints");
   coop_launch(c, (const void*)dev::k_cg, c.coop_cg_blocks, &a);
-  c.epoch += static_cast<int>(std::min<long long>(cfg.cg_max_iter, 1 << 28)) + 1;
   return read_status(c).cg;
 }
 
@@ -507,6 +538,8 @@ void upload_values(Ctx& c, const hykkt_values_t* v) {
   up(c.r_s, v->r_s, k.md, "r_s");
   up(c.r_y, v->r_y, k.mc, "r_y");
   up(c.r_yd, v->r_yd, k.md, "r_yd");
+  c.v = {c.hval.p, c.jval.p, c.jdval.p, c.d_x.p, c.d_s.p, c.r_tx.p, c.r_s.p, c.r_y.p, c.r_yd.p};
+  c.o = {c.dx.p, c.dy.p, c.ds.p, c.dyd.p};
   c.have_values = true;
 }
 
@@ -553,8 +586,8 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
   ev.rec(0, st);
   // ---- assembly: reduce, Ruiz, scale, H_gamma -------------------------
   const long long nred = std::max<long long>(ap.n_ht, ap.nx);
-  dev::k_reduce<<<blocks_for(nred), kThreads, 0, st>>>(ap, c.hval.p, c.jdval.p, c.d_x.p, c.d_s.p,
-                                                       c.r_tx.p, c.r_s.p, c.r_yd.p, c.ht.p, c.r_x.p);
+  dev::k_reduce<<<blocks_for(nred), kThreads, 0, st>>>(ap, c.v.h, c.v.jd, c.v.dx, c.v.ds,
+                                                       c.v.rtx, c.v.rs, c.v.ryd, c.ht.p, c.r_x.p);
   check_launch(c);
   c.ruiz_flags.alloc(cfg.ruiz_max_iters + 2);
   CK(cudaMemsetAsync(c.ruiz_flags.p, 0, sizeof(int) * (cfg.ruiz_max_iters + 2), st));
@@ -563,7 +596,7 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
     dev::RuizArgs ra;
     ra.p = ap;
     ra.ht = c.ht.p;
-    ra.jval = c.jval.p;
+    ra.jval = c.v.j;
     ra.d = c.dscale.p;
     ra.norms = c.norms.p;
     ra.unconverged = c.ruiz_flags.p;
@@ -575,7 +608,7 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
     coop_launch(c, (const void*)dev::k_ruiz, c.coop_ruiz_blocks, &ra);
   }
   const long long nsc = std::max<long long>({(long long)ap.n_ht, (long long)ap.nnz_j, (long long)ap.nx, (long long)ap.mc});
-  dev::k_scale<<<blocks_for(nsc), kThreads, 0, st>>>(ap, c.dscale.p, c.ht.p, c.jval.p, c.r_x.p, c.r_y.p,
+  dev::k_scale<<<blocks_for(nsc), kThreads, 0, st>>>(ap, c.dscale.p, c.ht.p, c.v.j, c.r_x.p, c.v.ry,
                                                      c.hts.p, c.js.p, c.js_csr.p, c.rxs.p, c.rys.p);
   check_launch(c);
   CK(cudaMemsetAsync(c.maxdiag.p, 0, sizeof(double), st));
@@ -627,7 +660,7 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
   run_trsv(c, c.rhat.p, nullptr, c.js.p, nullptr);
   if (k.mc > 0) {
     dev::k_schur_rhs<<<blocks_for(k.mc), kThreads, 0, st>>>(static_cast<int>(k.mc), c.jcsr_rp.p, c.jcsr_ci_perm.p,
-                                                           c.js_csr.p, c.y.p, c.rys.p, c.cg_rhs.p);
+                                                           c.js_csr.p, c.xsol.p, c.rys.p, c.cg_rhs.p);
     check_launch(c);
   }
   ev.rec(3, st);
@@ -660,8 +693,8 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
   {
     const long long nrec = std::max<long long>({(long long)k.nx, (long long)k.mc, (long long)k.md});
     dev::k_recover<<<blocks_for(nrec), kThreads, 0, st>>>(ap, c.jdcsr_rp.p, c.jdcsr_ci.p, c.jdcsr_src.p, c.dscale.p,
-                                                          c.dx_s.p, c.cg_x.p, c.jdval.p, c.d_s.p, c.r_s.p, c.r_yd.p,
-                                                          c.dx.p, c.dy.p, c.ds.p, c.dyd.p);
+                                                          c.dx_s.p, c.cg_x.p, c.v.jd, c.v.ds, c.v.rs, c.v.ryd,
+                                                          c.o.dx, c.o.dy, c.o.ds, c.o.dyd);
     check_launch(c);
   }
   ev.rec(5, st);
@@ -689,18 +722,18 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
 
   if (flags & HYKKT_FLAG_METRICS) {
     const idx nx = k.nx, mc = k.mc, md = k.md;
-    auto dl = [&](const hykkt::DBuf<double>& b, idx n) {
+    auto dl = [&](const double* src, idx n) {
       std::vector<double> h(n);
-      if (n) CK(cudaMemcpy(h.data(), b.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+      if (n) CK(cudaMemcpy(h.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost));
       return h;
     };
-    const auto hv = dl(c.hval, k.h.nnz()), jv = dl(c.jval, k.j.nnz()), jdv = dl(c.jdval, k.jd.nnz());
-    const auto dxv = dl(c.d_x, nx), dsv = dl(c.d_s, md), rtx = dl(c.r_tx, nx), rs = dl(c.r_s, md),
-               ry = dl(c.r_y, mc), ryd = dl(c.r_yd, md);
-    const auto htv = dl(c.ht, k.ht.nnz()), htsv = dl(c.hts, k.ht.nnz()), jsv = dl(c.js, k.j.nnz());
-    const auto rx = dl(c.r_x, nx), rxs = dl(c.rxs, nx), rys = dl(c.rys, mc);
-    const auto sdx = dl(c.dx_s, nx), sdy = dl(c.cg_x, mc);
-    const auto odx = dl(c.dx, nx), ody = dl(c.dy, mc), ods = dl(c.ds, md), odyd = dl(c.dyd, md);
+    const auto hv = dl(c.v.h, k.h.nnz()), jv = dl(c.v.j, k.j.nnz()), jdv = dl(c.v.jd, k.jd.nnz());
+    const auto dxv = dl(c.v.dx, nx), dsv = dl(c.v.ds, md), rtx = dl(c.v.rtx, nx), rs = dl(c.v.rs, md),
+               ry = dl(c.v.ry, mc), ryd = dl(c.v.ryd, md);
+    const auto htv = dl(c.ht.p, k.ht.nnz()), htsv = dl(c.hts.p, k.ht.nnz()), jsv = dl(c.js.p, k.j.nnz());
+    const auto rx = dl(c.r_x.p, nx), rxs = dl(c.rxs.p, nx), rys = dl(c.rys.p, mc);
+    const auto sdx = dl(c.dx_s.p, nx), sdy = dl(c.cg_x.p, mc);
+    const auto odx = dl(c.o.dx, nx), ody = dl(c.o.dy, mc), ods = dl(c.o.ds, md), odyd = dl(c.o.dyd, md);
     const CscView H{nx, nx, k.h.cp.data(), k.h.ri.data(), hv.data()};
     const CscView J{mc, nx, k.j.cp.data(), k.j.ri.data(), jv.data()};
     const CscView JD{md, nx, k.jd.cp.data(), k.jd.ri.data(), jdv.data()};
@@ -723,13 +756,104 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
 
 void download_solution(Ctx& c, double* dx, double* ds, double* dy, double* dyd) {
   const KktPlan& k = c.kp;
-  auto dl = [&](const hykkt::DBuf<double>& b, double* out, idx n) {
-    if (out && n) CK(cudaMemcpyAsync(out, b.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  auto dl = [&](const double* src, double* out, idx n) {
+    if (out && n) CK(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
   };
-  dl(c.dx, dx, k.nx);
-  dl(c.ds, ds, k.md);
-  dl(c.dy, dy, k.mc);
-  dl(c.dyd, dyd, k.md);
+  dl(c.o.dx, dx, k.nx);
+  dl(c.o.ds, ds, k.md);
+  dl(c.o.dy, dy, k.mc);
+  dl(c.o.dyd, dyd, k.md);
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+// ---- resident batch: B systems on the analysed pattern ----------------------
+// Values are kept field-major on the device ([field][system][entry]); the
+// systems are solved back to back through the single-system path, each with
+// a fresh RegularizationState (the reference's independent-matrix mode,
+// solver.cpp:374-398).
+struct BatchLayout {
+  idx sizes[9];
+  idx total_per_sys;
+};
+
+BatchLayout batch_layout(const KktPlan& k) {
+  BatchLayout L;
+  const idx s[9] = {k.h.nnz(), k.j.nnz(), k.jd.nnz(), k.nx, k.md, k.nx, k.md, k.mc, k.md};
+  L.total_per_sys = 0;
+  for (int i = 0; i < 9; ++i) {
+    L.sizes[i] = s[i];
+    L.total_per_sys += s[i];
+  }
+  return L;
+}
+
+void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v) {
+  if (!c.have_kkt) throw StateError("hykkt_analyze must be called first");
+  if (batch <= 0) throw InvalidArgument("batch must be positive");
+  if (!v) throw InvalidArgument("null values");
+  const BatchLayout L = batch_layout(c.kp);
+  c.bvals.alloc(static_cast<std::size_t>(batch * L.total_per_sys));
+  const double* src[9] = {v->h_val, v->j_val, v->jd_val, v->d_x, v->d_s, v->r_tilde_x, v->r_s, v->r_y, v->r_yd};
+  idx off = 0;
+  for (int i = 0; i < 9; ++i) {
+    const idx n = batch * L.sizes[i];
+    if (n > 0 && !src[i]) throw InvalidArgument("null value array in batch upload");
+    if (n > 0) CK(cudaMemcpyAsync(c.bvals.p + off, src[i], n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    off += n;
+  }
+  const idx nout = c.kp.nx + c.kp.mc + 2 * c.kp.md;
+  c.bouts.alloc(static_cast<std::size_t>(batch * nout));
+  c.batch = batch;
+  c.batch_reports.assign(batch, hykkt_report_t{});
+}
+
+void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_report_t* reports) {
+  if (c.batch <= 0) throw StateError("no batch uploaded");
+  const BatchLayout L = batch_layout(c.kp);
+  const KktPlan& k = c.kp;
+  hykkt_timing_t sum{};
+  for (idx b = 0; b < c.batch; ++b) {
+    double* f[9];
+    idx off = 0;
+    for (int i = 0; i < 9; ++i) {
+      f[i] = c.bvals.p + off + b * L.sizes[i];
+      off += c.batch * L.sizes[i];
+    }
+    c.v = {f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], f[8]};
+    double* o = c.bouts.p;
+    c.o = {o + b * k.nx, o + c.batch * k.nx + b * k.mc, o + c.batch * (k.nx + k.mc) + b * k.md,
+           o + c.batch * (k.nx + k.mc + k.md) + b * k.md};
+    c.have_values = true;
+    double dmin = 0.0;  // fresh RegularizationState per system
+    hykkt_report_t r{};
+    solve_resident(c, cfg, &dmin, flags, &r);
+    c.batch_reports[b] = r;
+    if (reports) reports[b] = r;
+    sum.assemble_ms += c.timing.assemble_ms;
+    sum.factor_ms += c.timing.factor_ms;
+    sum.solve_w_ms += c.timing.solve_w_ms;
+    sum.cg_ms += c.timing.cg_ms;
+    sum.solve_dx_ms += c.timing.solve_dx_ms;
+    sum.total_ms += c.timing.total_ms;
+    sum.kernel_launches += c.timing.kernel_launches;
+    sum.cg_kernel_launches += c.timing.cg_kernel_launches;
+  }
+  c.timing = sum;
+  c.have_values = false;  // c.v points into the batch; single-system values must be re-uploaded
+}
+
+void batch_download(Ctx& c, double* dx, double* ds, double* dy, double* dyd) {
+  if (c.batch <= 0) throw StateError("no batch uploaded");
+  const KktPlan& k = c.kp;
+  const idx B = c.batch;
+  auto dl = [&](const double* src, double* out, idx n) {
+    if (out && n) CK(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  };
+  const double* o = c.bouts.p;
+  dl(o, dx, B * k.nx);
+  dl(o + B * k.nx, dy, B * k.mc);
+  dl(o + B * (k.nx + k.mc), ds, B * k.md);
+  dl(o + B * (k.nx + k.mc + k.md), dyd, B * k.md);
   CK(cudaStreamSynchronize(c.stream));
 }
 
@@ -816,16 +940,11 @@ int hykkt_analyze(hykkt_t h, int64_t n_x, int64_t m_c, int64_t m_d, const int64_
   });
 }
 
-int hykkt_analysis_info(hykkt_t h, hykkt_analysis_t* out) {
-  return guarded([&] {
-    Ctx& c = ctx(h);
-    if (!c.have_plan) throw StateError("no analysis");
-    if (!out) throw InvalidArgument("null output");
-    const SupernodalPlan& s = c.sp;
+static hykkt_analysis_t stats_of(const SupernodalPlan& s, const KktPlan* kp) {
     hykkt_analysis_t a{};
     a.n = s.n;
-    a.nnz_h_tilde = c.have_kkt ? c.kp.ht.nnz() : 0;
-    a.nnz_h_gamma = c.have_kkt ? c.kp.hg.nnz() : 0;
+    a.nnz_h_tilde = kp ? kp->ht.nnz() : 0;
+    a.nnz_h_gamma = kp ? kp->hg.nnz() : 0;
     a.nnz_l = s.l_nnz();
     a.n_supernodes = s.nsup;
     a.n_levels = s.nlevels;
@@ -840,11 +959,36 @@ int hykkt_analysis_info(hykkt_t h, hykkt_analysis_t* out) {
     a.max_sn_rows = s.max_nrows;
     a.panel_slots = s.panel_size;
     a.factor_flops = s.factor_flops;
-    a.nnz_j = c.have_kkt ? c.kp.j.nnz() : 0;
-    a.nnz_jd = c.have_kkt ? c.kp.jd.nnz() : 0;
-    a.m_c = c.have_kkt ? c.kp.mc : 0;
-    a.m_d = c.have_kkt ? c.kp.md : 0;
-    *out = a;
+    a.nnz_j = kp ? kp->j.nnz() : 0;
+    a.nnz_jd = kp ? kp->jd.nnz() : 0;
+    a.m_c = kp ? kp->mc : 0;
+    a.m_d = kp ? kp->md : 0;
+    return a;
+}
+
+int hykkt_analysis_info(hykkt_t h, hykkt_analysis_t* out) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_plan) throw StateError("no analysis");
+    if (!out) throw InvalidArgument("null output");
+    *out = stats_of(c.sp, c.have_kkt ? &c.kp : nullptr);
+  });
+}
+
+int hykkt_host_analyze(int64_t n_x, int64_t m_c, int64_t m_d, const int64_t* h_colptr,
+                       const int64_t* h_rowidx, const int64_t* j_colptr, const int64_t* j_rowidx,
+                       const int64_t* jd_colptr, const int64_t* jd_rowidx, const int64_t* perm,
+                       int64_t* perm_out, hykkt_analysis_t* out) {
+  return guarded([&] {
+    if (n_x < 0 || m_c < 0 || m_d < 0) throw InvalidArgument("negative dimension");
+    KktPlan kp = build_kkt_plan(n_x, m_c, m_d, pattern_from(n_x, n_x, h_colptr, h_rowidx),
+                                pattern_from(m_c, n_x, j_colptr, j_rowidx),
+                                pattern_from(m_d, n_x, jd_colptr, jd_rowidx));
+    std::vector<idx> pv;
+    if (perm) pv.assign(perm, perm + n_x);
+    const SupernodalPlan sp = build_supernodal_plan(kp.hg, std::move(pv));
+    if (perm_out) std::copy(sp.perm.begin(), sp.perm.end(), perm_out);
+    if (out) *out = stats_of(sp, &kp);
   });
 }
 
@@ -973,6 +1117,70 @@ int hykkt_chol_get_factor(hykkt_t h, int64_t* l_colptr, int64_t* l_rowidx, doubl
       if (s.panel_size) CK(cudaMemcpy(pan.data(), c.panel.p, s.panel_size * sizeof(double), cudaMemcpyDeviceToHost));
       for (std::size_t q = 0; q < s.l_to_panel.size(); ++q) l_values[q] = pan[s.l_to_panel[q]];
     }
+  });
+}
+
+// Diagnostics: supernode structure (order, first column, rows, parent).
+int hykkt_debug_plan(hykkt_t h, int32_t* order, int32_t* first, int32_t* nrows, int32_t* parent) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_plan) throw StateError("no analysis");
+    const SupernodalPlan& s = c.sp;
+    std::copy(s.order.begin(), s.order.end(), order);
+    std::copy(s.sn_first.begin(), s.sn_first.end(), first);
+    std::copy(s.sn_nrows.begin(), s.sn_nrows.end(), nrows);
+    std::copy(s.sn_parent.begin(), s.sn_parent.end(), parent);
+  });
+}
+
+// Diagnostics: one traced H^-1 pass (b = r_hat_x of the last KKT solve);
+// out[t] / out[2 nsup + t] = end / start time (ns) of task t (t < nsup:
+// forward task of order[t]; else backward task of order[2 nsup - 1 - t]).
+int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_factor || !c.have_kkt) throw StateError("needs a factored KKT system");
+    const idx ns = c.sp.nsup;
+    hykkt::DBuf<unsigned long long> tr;
+    tr.alloc(6 * ns);
+    dev::TrsvArgs ta = trsv_args(c);
+    ta.rhs.b = c.rhat.p;
+    ta.trace = tr.p;
+    coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
+    read_status(c);
+    CK(cudaMemcpy(out, tr.p, 6 * ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int hykkt_batch_upload(hykkt_t h, int64_t batch, const hykkt_values_t* values) {
+  return guarded([&] { batch_upload(ctx(h), batch, values); });
+}
+
+int hykkt_batch_solve_resident(hykkt_t h, const hykkt_config_t* cfg, int flags, hykkt_report_t* reports) {
+  return guarded([&] {
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    batch_solve_resident(ctx(h), cfg ? *cfg : d, flags, reports);
+  });
+}
+
+int hykkt_batch_download(hykkt_t h, double* dx, double* ds, double* dy, double* dyd) {
+  return guarded([&] { batch_download(ctx(h), dx, ds, dy, dyd); });
+}
+
+int hykkt_batch_solve(hykkt_t h, const hykkt_config_t* cfg, int64_t batch, const hykkt_values_t* values,
+                      int flags, hykkt_report_t* reports, double* dx, double* ds, double* dy, double* dyd) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    batch_upload(c, batch, values);
+    batch_solve_resident(c, cfg ? *cfg : d, flags, reports);
+    batch_download(c, dx, ds, dy, dyd);
   });
 }
 

@@ -43,6 +43,13 @@ struct SnPlan {
   const int* lrow_pos;
   const int* perm;
   const int* iperm;
+  const int* u_off;
+  const int* ext_ptr;
+  const int* ext_map;
+  const int* gat_ptr;
+  const int* gat_idx;
+  const int* relind;
+  int u_size;
 };
 
 struct FactorArgs {
@@ -77,7 +84,6 @@ __device__ void factor_task(const FactorArgs& a, int sn, int lane, double floor_
       if (!wait_flag(a.done + s.child[c], a.epoch, a.abort)) break;
     }
     __syncwarp();
-    __threadfence();
     ok = ld_relaxed(a.fail_col) >= f && !ld_relaxed(a.abort);
   }
   if (ok) {
@@ -124,9 +130,7 @@ __device__ void factor_task(const FactorArgs& a, int sn, int lane, double floor_
       __syncwarp();
     }
   }
-  __syncwarp();
-  __threadfence();
-  if (lane == 0) st_release(a.done + sn, a.epoch);
+  warp_publish(a.done + sn, a.epoch, lane);
 }
 
 __global__ void __launch_bounds__(256) k_factor(FactorArgs a) {

@@ -32,114 +32,340 @@ struct SolveRhs {
   const double* jval;
 };
 
+// Unset-value marker: a signalling-NaN bit pattern that arithmetic never
+// produces.  y (forward result) and x (backward result) are reset to it
+// before each pass; a consumer spins on the VALUE it needs, so the data is
+// its own completion flag — no per-task flags, no fences on the hot path.
+constexpr long long kUnset = 0x7FF4DEADBEEF0001ll;
+
+__device__ __forceinline__ double poll_value(const double* p, int* abort) {
+  double v = ldcg(p);
+  if (__double_as_longlong(v) != kUnset) return v;
+  const long long t0 = clock64();
+  for (unsigned it = 1;; ++it) {
+    __nanosleep(16);
+    v = ldcg(p);
+    if (__double_as_longlong(v) != kUnset) return v;
+    if ((it & 255u) == 0u) {
+      if (ld_relaxed(abort)) return 0.0;
+      if (clock64() - t0 > kSpinBudget) {
+        atomicExch(abort, 1);
+        return 0.0;
+      }
+    }
+  }
+}
+
+// Load a value that is expected to be set; poll only if it is not yet.
+__device__ __forceinline__ double load_ready(const double* p, int* abort) {
+  const double v = ldcg(p);
+  return __double_as_longlong(v) != kUnset ? v : poll_value(p, abort);
+}
+
 struct TrsvArgs {
   SnPlan s;
   const double* panel;
-  double* y;       // permuted work vector, holds the solution afterwards
+  double* y;       // forward result (permuted), reset to kUnset per pass
+  double* x;       // backward result (permuted), reset to kUnset per pass
+  double* u;       // update vectors (SnPlan::u_off), reset to kUnset per pass
+  double* acc_buf; // per-supernode accumulators for wide supernodes
   double* x_out;   // original-order output or null
-  int* fdone;
-  int* bdone;
-  int epoch;
   int* abort;
   SolveRhs rhs;
+  GridBarrier bar;
+  unsigned long long* trace;  // diagnostics: per-task end / start times (ns)
 };
 
-__device__ void fwd_task(const TrsvArgs& a, int sn, int lane) {
-  const SnPlan& s = a.s;
-  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
-  const double* P = a.panel + s.off[sn];
-  for (int c = s.child_ptr[sn] + lane; c < s.child_ptr[sn + 1]; c += 32) {
-    if (!wait_flag(a.fdone + s.child[c], a.epoch, a.abort)) break;
-  }
-  __syncwarp();
-  __threadfence();
-  for (int cb = 0; cb < w; cb += 32) {
-    const int cw = min(32, w - cb);
-    double acc = 0.0;
-    if (lane < cw) {
-      const int o = s.perm[f + cb + lane];
-      double bi = a.rhs.b ? a.rhs.b[o] : 0.0;
-      if (a.rhs.u) {
-        double t = 0.0;  // spmv(J, u, transpose) order, csc_matrix.cpp:255-261
-        for (int q = a.rhs.j_cp[o]; q < a.rhs.j_cp[o + 1]; ++q) {
-          t = __dadd_rn(t, __dmul_rn(a.rhs.jval[q], ldcg(a.rhs.u + a.rhs.j_ri[q])));
-        }
-        bi = a.rhs.b ? __dsub_rn(bi, t) : t;
-      }
-      acc = bi;
-    }
-    for (int rr = 0; rr < cw; ++rr) {
-      const int i = f + cb + rr;
-      double part = 0.0;
-      for (int e = s.lrow_ptr[i] + lane; e < s.lrow_ptr[i + 1]; e += 32) {
-        part = fma(__ldg(a.panel + s.lrow_pos[e]), ldcg(a.y + s.lrow_col[e]), part);
-      }
-      for (int k = lane; k < cb; k += 32) part = fma(__ldg(P + k * nr + cb + rr), ldcg(a.y + f + k), part);
-      part = warp_sum(part);
-      if (lane == rr) acc -= part;
-    }
-    for (int k = 0; k < cw; ++k) {
-      const double yk = __shfl_sync(0xffffffffu, acc, k) / __ldg(P + (cb + k) * nr + cb + k);
-      if (lane == k) acc = yk;
-      if (lane > k && lane < cw) acc = fma(-__ldg(P + (cb + k) * nr + cb + lane), yk, acc);
-    }
-    if (lane < cw) stcg(a.y + f + cb + lane, acc);
-    __syncwarp();
-  }
-  __threadfence();
-  if (lane == 0) st_release(a.fdone + sn, a.epoch);
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-__device__ void bwd_task(const TrsvArgs& a, int sn, int lane) {
+__device__ __forceinline__ void reset_unset(double* v, int n) {
+  const double u = __longlong_as_double(kUnset);
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int i = gt; i < n; i += gs) v[i] = u;
+}
+
+// Right-hand side entry of permuted row i: b[perm i] and/or J^T u in the
+// reference's spmv(J, u, transpose) order (csc_matrix.cpp:255-261).
+__device__ __forceinline__ double rhs_at(const TrsvArgs& a, int i) {
+  const int o = a.s.perm[i];
+  double bi = a.rhs.b ? a.rhs.b[o] : 0.0;
+  if (a.rhs.u) {
+    double t = 0.0;
+    for (int q = a.rhs.j_cp[o]; q < a.rhs.j_cp[o + 1]; ++q) {
+      t = __dadd_rn(t, __dmul_rn(a.rhs.jval[q], ldcg(a.rhs.u + a.rhs.j_ri[q])));
+    }
+    bi = a.rhs.b ? __dsub_rn(bi, t) : t;
+  }
+  return bi;
+}
+
+// Sum of u[gat_idx[g]] for g in [gb, ge) in list order, four loads in
+// flight; only values still unset are polled.
+__device__ __forceinline__ double gather_u(const TrsvArgs& a, int gb, int ge) {
+  double v = 0.0;
+  for (int g = gb; g < ge; g += 4) {
+    int i[4];
+    double x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) i[k] = (g + k < ge) ? __ldg(a.s.gat_idx + g + k) : -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = i[k] >= 0 ? ldcg(a.u + i[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i[k] >= 0 && __double_as_longlong(x[k]) == kUnset) x[k] = poll_value(a.u + i[k], a.abort);
+      v += x[k];
+    }
+  }
+  return v;
+}
+
+// One lane per child polls the child's last update-vector entry; the rest
+// of the warp sleeps at the barrier instead of flooding the SM's L1TEX queue
+// with one poll per lane.  Values are re-checked when actually loaded.
+__device__ __forceinline__ void wait_children(const TrsvArgs& a, int sn, int lane) {
+  const SnPlan& s = a.s;
+  for (int c = s.child_ptr[sn] + lane; c < s.child_ptr[sn + 1]; c += 32) {
+    const int ch = s.child[c];
+    poll_value(a.u + s.u_off[ch + 1] - 1, a.abort);
+  }
+  __syncwarp();
+}
+
+// Forward task, multifrontal form: acc = sum of children's update vectors
+// (extend-add through flattened gather lists), own rows:
+// y = L_ss^-1 (b - acc), rows below: u_s = acc + L_below y, handed to the
+// parent.  Every static load (gather indices, L, right-hand side) is issued
+// before the first wait, so a tree level costs about one L2 round trip.
+__device__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
+  const SnPlan& s = a.s;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const int rp = s.rows_ptr[sn];
+  const double* P = a.panel + s.off[sn];
+  double* U = a.u + s.u_off[sn];
+  if (nr <= 32 && w <= 4) {
+    // Narrow supernode: lane q owns row-structure position q.
+    const bool own = lane < w, row = lane < nr;
+    int gb = 0, ge = 0;
+    if (row) {
+      gb = __ldg(s.gat_ptr + rp + lane);
+      ge = __ldg(s.gat_ptr + rp + lane + 1);
+    }
+    int gi[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gi[k] = (gb + k < ge) ? __ldg(s.gat_idx + gb + k) : -1;
+    double lrow[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lrow[k] = (row && k < w) ? __ldg(P + k * nr + lane) : 0.0;
+    const double bi = own ? rhs_at(a, f + lane) : 0.0;
+    wait_children(a, sn, lane);
+    double xv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xv[k] = gi[k] >= 0 ? ldcg(a.u + gi[k]) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (gi[k] >= 0 && __double_as_longlong(xv[k]) == kUnset) xv[k] = poll_value(a.u + gi[k], a.abort);
+      acc += xv[k];
+    }
+    if (ge - gb > 4) acc += gather_u(a, gb + 4, ge);
+    acc = own ? bi - acc : acc;
+    if (a.trace) { __syncwarp(); if (lane == 0) a.trace[4 * a.s.nsup + tslot] = global_ns(); }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < w) {
+        const double yk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, lrow[k], k);
+        if (lane == k) acc = yk;
+        if (lane > k && lane < w) acc = fma(-lrow[k], yk, acc);
+        if (lane >= w && row) acc = fma(lrow[k], yk, acc);
+      }
+    }
+    if (own) stcg(a.y + f + lane, acc);
+    if (lane >= w && row) stcg(U + lane - w, acc);
+    return;
+  }
+  // General supernode: A[q] (per-supernode scratch) holds, for own rows,
+  // b - (children's contributions) and for rows below, the running update.
+  double* A = a.acc_buf + rp;
+  for (int q = lane; q < nr; q += 32) A[q] = q < w ? rhs_at(a, f + q) : 0.0;
+  wait_children(a, sn, lane);
+  // Extend-add the children's update vectors (child-side relative indices:
+  // coalesced, four loads in flight per lane).
+  for (int c = s.child_ptr[sn]; c < s.child_ptr[sn + 1]; ++c) {
+    const int ch = s.child[c];
+    const int m = s.nrows[ch] - (s.first[ch + 1] - s.first[ch]);
+    const double* uc = a.u + s.u_off[ch];
+    const int* rel = s.relind + s.u_off[ch];
+    for (int tb = 0; tb < m; tb += 128) {
+      int q[4];
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = tb + lane + 32 * j;
+        q[j] = t < m ? __ldg(rel + t) : -1;
+        v[j] = t < m ? ldcg(uc + t) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (q[j] >= 0) {
+          if (__double_as_longlong(v[j]) == kUnset) v[j] = poll_value(uc + tb + lane + 32 * j, a.abort);
+          A[q[j]] += (q[j] < w) ? -v[j] : v[j];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  for (int cb = 0; cb < w; cb += 32) {
+    const int cw = min(32, w - cb);
+    double d[32];  // row cb+lane of the chunk's diagonal block, all loads in flight
+#pragma unroll
+    for (int k = 0; k < 32; ++k) d[k] = (k < cw && lane < cw) ? __ldg(P + (cb + k) * nr + cb + lane) : 0.0;
+    double acc = lane < cw ? A[cb + lane] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k < cw) {
+        const double yk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, d[k], k);
+        if (lane == k) acc = yk;
+        if (lane > k && lane < cw) acc = fma(-d[k], yk, acc);
+      }
+    }
+    if (lane < cw) stcg(a.y + f + cb + lane, acc);
+    for (int qb = cb + cw; qb < nr; qb += 32) {  // warp-uniform trip count
+      const int q = qb + lane;
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k < cw) {
+          const double yk = __shfl_sync(0xffffffffu, acc, k);
+          if (q < nr) t = fma(__ldg(P + (cb + k) * nr + q), yk, t);
+        }
+      }
+      if (q < nr) A[q] += (q < w) ? -t : t;
+    }
+    __syncwarp();
+  }
+  for (int q = w + lane; q < nr; q += 32) stcg(U + q - w, A[q]);
+}
+
+// The parent publishes its first column last; once it is visible every
+// ancestor value this task reads has been written.  One lane polls.
+__device__ __forceinline__ void wait_parent(const TrsvArgs& a, int sn, int lane) {
+  const int par = a.s.parent[sn];
+  if (lane == 0) poll_value(par >= 0 ? a.x + a.s.first[par] : a.y + a.s.first[sn], a.abort);
+  __syncwarp();
+}
+
+__device__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const double* P = a.panel + s.off[sn];
   const int* R = s.rows + s.rows_ptr[sn];
-  if (lane == 0) {
-    const int par = s.parent[sn];
-    if (par < 0) wait_flag(a.fdone + sn, a.epoch, a.abort);
-    else wait_flag(a.bdone + par, a.epoch, a.abort);
+  if (w <= 4 && nr - w <= 32) {
+    // Narrow: lane r owns below row w + r; lane l < w owns column l.
+    const int below = nr - w;
+    int gr = 0;
+    double lv[4], ld[4];
+    if (lane < below) gr = __ldg(R + w + lane);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lv[k] = (lane < below && k < w) ? __ldg(P + k * nr + w + lane) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ld[k] = (lane < w && k < w) ? __ldg(P + lane * nr + k) : 0.0;  // L(k, lane)
+    wait_parent(a, sn, lane);
+    double acc = lane < w ? load_ready(a.y + f + lane, a.abort) : 0.0;
+    const double xr = lane < below ? load_ready(a.x + gr, a.abort) : 0.0;
+    if (a.trace) { __syncwarp(); if (lane == 0) a.trace[4 * a.s.nsup + tslot] = global_ns(); }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < w) {
+        const double t = warp_sum(lv[k] * xr);
+        if (lane == k) acc -= t;
+      }
+    }
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      if (k < w) {
+        const double xk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, ld[k], k);
+        if (lane == k) acc = xk;
+        if (lane < k) acc = fma(-ld[k], xk, acc);
+      }
+    }
+    if (lane < w) {
+      stcg(a.x + f + lane, acc);
+      if (a.x_out) a.x_out[s.perm[f + lane]] = acc;
+    }
+    return;
   }
-  __syncwarp();
-  __threadfence();
   const int nchunks = (w + 31) >> 5;
   for (int ci = nchunks - 1; ci >= 0; --ci) {
     const int cb = ci * 32, cw = min(32, w - cb);
-    double acc = (lane < cw) ? ldcg(a.y + f + cb + lane) : 0.0;
-    for (int kk = 0; kk < cw; ++kk) {
-      const double* Pc = P + (cb + kk) * nr;
-      double part = 0.0;
-      for (int r = cb + cw + lane; r < nr; r += 32) part = fma(__ldg(Pc + r), ldcg(a.y + __ldg(R + r)), part);
-      part = warp_sum(part);
-      if (lane == kk) acc -= part;
+    double d[32];  // column cb+lane of the chunk's diagonal block: L(cb+k, cb+lane)
+#pragma unroll
+    for (int k = 0; k < 32; ++k) d[k] = (k < cw && lane < cw) ? __ldg(P + (cb + lane) * nr + cb + k) : 0.0;
+    if (ci == nchunks - 1) wait_parent(a, sn, lane);
+    double acc = lane < cw ? load_ready(a.y + f + cb + lane, a.abort) : 0.0;
+    const int rb0 = cb + cw;  // rows below this chunk (own later chunks + ancestors)
+    double t = 0.0;           // lane = column: sum_r L(r, cb+lane) x_r
+    for (int rb = rb0; rb < nr; rb += 32) {
+      const int r = rb + lane;
+      const double xr = r < nr ? load_ready(a.x + __ldg(R + r), a.abort) : 0.0;
+#pragma unroll
+      for (int qq = 0; qq < 32; ++qq) {
+        const double xq = __shfl_sync(0xffffffffu, xr, qq);
+        if (lane < cw && rb + qq < nr) t = fma(__ldg(P + (cb + lane) * nr + rb + qq), xq, t);
+      }
     }
-    for (int k = cw - 1; k >= 0; --k) {
-      const double xk = __shfl_sync(0xffffffffu, acc, k) / __ldg(P + (cb + k) * nr + cb + k);
-      if (lane == k) acc = xk;
-      if (lane < k) acc = fma(-__ldg(P + (cb + lane) * nr + cb + k), xk, acc);
+    acc -= t;
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      if (k < cw) {
+        const double xk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, d[k], k);
+        if (lane == k) acc = xk;
+        if (lane < k) acc = fma(-d[k], xk, acc);
+      }
     }
     if (lane < cw) {
-      stcg(a.y + f + cb + lane, acc);
+      stcg(a.x + f + cb + lane, acc);
       if (a.x_out) a.x_out[s.perm[f + cb + lane]] = acc;
     }
     __syncwarp();
   }
-  __threadfence();
-  if (lane == 0) st_release(a.bdone + sn, a.epoch);
 }
 
+// One forward + backward pass; y and x must hold kUnset on entry.
 __device__ __forceinline__ void trsv_pass(const TrsvArgs& a) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int ns = a.s.nsup;
   for (int t = gw; t < 2 * ns; t += nw) {
-    if (t < ns) fwd_task(a, a.s.order[t], lane);
-    else bwd_task(a, a.s.order[2 * ns - 1 - t], lane);
+    if (a.trace && lane == 0) a.trace[2 * ns + t] = global_ns();
+    if (t < ns) fwd_task(a, a.s.order[t], lane, t);
+    else bwd_task(a, a.s.order[2 * ns - 1 - t], lane, t);
+    if (a.trace && lane == 0) a.trace[t] = global_ns();
   }
 }
 
-__global__ void __launch_bounds__(256) k_trsv(TrsvArgs a) { trsv_pass(a); }
+__device__ __forceinline__ void rearm(const TrsvArgs& a) {
+  reset_unset(a.y, a.s.n);
+  reset_unset(a.x, a.s.n);
+  reset_unset(a.u, a.s.u_size);
+}
+
+__global__ void __launch_bounds__(256) k_trsv(TrsvArgs a) {
+  rearm(a);
+  grid_sync(a.bar, a.abort);
+  trsv_pass(a);
+}
+
+// L values in forward row-list order (after a successful factorization).
+__global__ void k_gather_lrow(int nnz, const int* __restrict__ pos, const double* __restrict__ panel,
+                              double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nnz) out[e] = panel[pos[e]];
+}
 
 // q = J t - r_y style products: out[k] = sum_e J_csr[e] * y[ci_perm[e]]
 // (+ sub[k] subtracted), reference spmv scatter order (csc_matrix.cpp:250-254,
@@ -171,7 +397,7 @@ struct CgResultDev {
 };
 
 struct CgArgs {
-  TrsvArgs tr;  // rhs.u must point at p
+  TrsvArgs tr;  // rhs.u must point at p; tr.bar is the grid barrier
   int mc;
   const int* jcsr_rp;
   const int* jcsr_ci_perm;
@@ -186,9 +412,7 @@ struct CgArgs {
   double tol;
   double thr;
   long long max_iter;
-  int epoch_base;
   CgResultDev* res;
-  GridBarrier bar;
 };
 
 // Deterministic all-blocks reduction of partials[b * 4 + slot].
@@ -203,6 +427,8 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int gs = gridDim.x * blockDim.x;
   int* abort = a.tr.abort;
+  const GridBarrier bar = a.tr.bar;
+  rearm(a.tr);
   double ss = 0.0;
   for (int k = gt; k < a.mc; k += gs) {
     const double v = a.rhs[k];
@@ -213,7 +439,7 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
   }
   ss = block_sum(ss, scratch);
   if (threadIdx.x == 0) a.partials[blockIdx.x * 4] = ss;
-  grid_sync(a.bar, abort);
+  grid_sync(bar, abort);
   const double rhs_norm = sqrt(reduce_partials(a.partials, 0, scratch));
   const bool writer = gt == 0;
   if (rhs_norm == 0.0) {
@@ -222,14 +448,13 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
   }
   double rho = rhs_norm * rhs_norm;
   double r_norm = rhs_norm;
-  TrsvArgs tr = a.tr;
+  const TrsvArgs& tr = a.tr;
   for (long long it = 1; it <= a.max_iter; ++it) {
-    tr.epoch = a.epoch_base + static_cast<int>(it);
     trsv_pass(tr);
-    grid_sync(a.bar, abort);
+    grid_sync(bar, abort);
     double pq = 0.0, pp = 0.0;
     for (int k = gt; k < a.mc; k += gs) {
-      double qk = j_row_dot(k, a.jcsr_rp, a.jcsr_ci_perm, a.jcsr, tr.y);
+      double qk = j_row_dot(k, a.jcsr_rp, a.jcsr_ci_perm, a.jcsr, tr.x);
       const double pk = ldcg(a.p + k);
       if (a.delta2 != 0.0) qk = __dadd_rn(qk, __dmul_rn(a.delta2, pk));
       a.q[k] = qk;
@@ -242,7 +467,7 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
       a.partials[blockIdx.x * 4 + 1] = pq;
       a.partials[blockIdx.x * 4 + 2] = pp;
     }
-    grid_sync(a.bar, abort);
+    grid_sync(bar, abort);
     const double curvature = reduce_partials(a.partials, 1, scratch);
     const double p_norm2 = reduce_partials(a.partials, 2, scratch);
     if (curvature <= a.thr * p_norm2 || ld_relaxed(abort)) {
@@ -250,6 +475,7 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
       return;
     }
     const double alpha = rho / curvature;
+    rearm(tr);  // q no longer needs x: re-arm for the next pass
     double rr = 0.0;
     for (int k = gt; k < a.mc; k += gs) {
       a.x[k] = __dadd_rn(a.x[k], __dmul_rn(alpha, ldcg(a.p + k)));
@@ -259,7 +485,7 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
     }
     rr = block_sum(rr, scratch);
     if (threadIdx.x == 0) a.partials[blockIdx.x * 4 + 3] = rr;
-    grid_sync(a.bar, abort);
+    grid_sync(bar, abort);
     r_norm = sqrt(reduce_partials(a.partials, 3, scratch));
     const double relres = r_norm / rhs_norm;
     if (relres <= a.tol) {
@@ -276,7 +502,7 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
     for (int k = gt; k < a.mc; k += gs) {
       a.p[k] = __dadd_rn(a.r[k], __dmul_rn(beta, a.p[k]));
     }
-    grid_sync(a.bar, abort);
+    grid_sync(bar, abort);
   }
   if (writer) *a.res = CgResultDev{0, r_norm / rhs_norm, 0, 0};
 }

@@ -316,3 +316,72 @@ class CholeskyFactor:
         lv = np.zeros(nnz) if self.ok else None
         check(_lib.lib().hykkt_chol_get_factor(self.dev.h, ip(cp), ip(ri), dp(lv), ip(par)))
         return dict(l_colptr=cp, l_rowidx=ri, l_values=lv, parent=par, perm=self.dev.perm())
+
+
+def host_analyze(sys: BlockKkt4x4, perm=None):
+    """Host-only symbolic analysis (no GPU): returns (stats dict, ordering)."""
+    a = [i64(x) for x in (sys.h.colptr, sys.h.rowidx, sys.j.colptr, sys.j.rowidx,
+                          sys.j_d.colptr, sys.j_d.rowidx)]
+    p = None if perm is None else i64(perm)
+    out = np.zeros(sys.n_x, np.int64)
+    st = _lib.Analysis()
+    check(_lib.lib().hykkt_host_analyze(sys.n_x, sys.m_c, sys.m_d, *[ip(x) for x in a], ip(p),
+                                        ip(out), C.byref(st)))
+    return {n: getattr(st, n) for n, _ in st._fields_}, out
+
+
+VALUE_FIELDS = ("h_val", "j_val", "jd_val", "d_x", "d_s", "r_tilde_x", "r_s", "r_y", "r_yd")
+
+
+def system_values(sys: BlockKkt4x4) -> tuple:
+    return (sys.h.values, sys.j.values, sys.j_d.values, sys.d_x, sys.d_s, sys.r_tilde_x,
+            sys.r_s, sys.r_y, sys.r_yd)
+
+
+def stack_values(systems: Sequence[BlockKkt4x4], out: dict | None = None) -> dict:
+    """[system][entry] arrays per value field (the batch C-ABI layout).  With
+    `out` (e.g. pinned host buffers) the arrays are filled in place."""
+    cols = list(zip(*[system_values(s) for s in systems]))
+    res = {}
+    for name, parts in zip(VALUE_FIELDS, cols):
+        if out is not None:
+            np.stack(parts, out=out[name])
+            res[name] = out[name]
+        else:
+            res[name] = np.ascontiguousarray(np.stack(parts), np.float64)
+    return res
+
+
+class Batch:
+    """B independent systems on the pattern analysed by `dev` (device-side
+    replacement of solve_sequence's parallel mode, solver.cpp:374-398)."""
+
+    def __init__(self, dev: Device):
+        self.dev = dev
+        self.count = 0
+
+    def upload(self, values: dict) -> None:
+        arrs = [values[n] for n in VALUE_FIELDS]
+        for a in arrs:
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise _lib.InvalidMatrixError(-1, "batch values must be C-contiguous float64")
+        self.count = arrs[0].shape[0]
+        self._keep = arrs
+        v = _lib.Values(*[dp(a) for a in arrs])
+        check(_lib.lib().hykkt_batch_upload(self.dev.h, self.count, C.byref(v)))
+
+    def solve_resident(self, cfg: SolverConfig, metrics: bool = False, timing: bool = False):
+        reps = (_lib.Report * self.count)()
+        flags = (_lib.FLAG_METRICS if metrics else 0) | (_lib.FLAG_TIMING if timing else 0)
+        check(_lib.lib().hykkt_batch_solve_resident(self.dev.h, C.byref(cfg.c()), flags, reps))
+        return [SolveReport.from_c(r) for r in reps]
+
+    def download(self, out: dict | None = None) -> dict:
+        s = self.dev._pattern
+        B = self.count
+        if out is None:
+            out = dict(dx=np.zeros((B, s.n_x)), ds=np.zeros((B, s.m_d)), dy=np.zeros((B, s.m_c)),
+                       dyd=np.zeros((B, s.m_d)))
+        check(_lib.lib().hykkt_batch_download(self.dev.h, dp(out["dx"]), dp(out["ds"]),
+                                              dp(out["dy"]), dp(out["dyd"])))
+        return out

@@ -112,3 +112,21 @@ def test_own_ordering_solves(ref):
     want = ref.solve_full(s, SolverConfig())
     assert rel(got.solution.stacked(), want.stacked()) <= 1e-8
     assert abs(got.report.cg_iterations - want.report["cg_iterations"]) <= 1
+
+
+def test_resident_batch_matches_reference(ref):
+    from paper_2110_03636_b200.solver import Batch, stack_values
+    systems = acopf.batch(120, 4, seed=7)
+    cfg = SolverConfig()
+    perm = ref.hgamma_amd(systems[0], cfg)
+    dev = Device(0)
+    dev.analyze(systems[0], perm)
+    b = Batch(dev)
+    b.upload(stack_values(systems))
+    reps = b.solve_resident(cfg)
+    out = b.download()
+    for k, s in enumerate(systems):
+        want = ref.solve_full(s, cfg, perm)
+        got = np.concatenate([out["dx"][k], out["ds"][k], out["dy"][k], out["dyd"][k]])
+        assert rel(got, want.stacked()) <= 1e-8
+        assert abs(reps[k].cg_iterations - want.report["cg_iterations"]) <= 1
