@@ -58,6 +58,7 @@ __device__ __forceinline__ void warp_publish(int* flag, int value, int lane) {
 // Values produced by other SMs inside the same launch are read through L2
 // (ld.global.cg); L1 is not coherent across SMs.
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ int ldcg_int(const int* p) { return __ldcg(p); }
 __device__ __forceinline__ void stcg(double* p, double v) { __stcg(p, v); }
 
 // Waits until *flag == want. Returns false (and raises *abort) on timeout
@@ -81,6 +82,16 @@ __device__ __forceinline__ bool wait_flag(const int* flag, int want, int* abort)
   }
   fence_gpu();
   return true;
+}
+
+// Dynamic task ticket: warps take tasks in topological order; a warp holds
+// at most one task, so the smallest unfinished task always has its
+// dependencies taken by running warps (deadlock-free) and a ready task is
+// never stuck behind a blocked one on the same warp.
+__device__ __forceinline__ long long grab_task(unsigned* ticket, int lane) {
+  unsigned t = 0;
+  if (lane == 0) t = atomicAdd(ticket, 1u);
+  return static_cast<long long>(__shfl_sync(0xffffffffu, t, 0));
 }
 
 struct GridBarrier {

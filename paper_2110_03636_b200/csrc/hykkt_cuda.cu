@@ -25,6 +25,7 @@
 #include "host_metrics.hpp"
 #include "kernels_assemble.cuh"
 #include "kernels_solve.cuh"
+#include "kernels_batch.cuh"
 
 namespace hykkt {
 
@@ -101,6 +102,7 @@ struct hykkt_context {
   cudaStream_t stream = nullptr;
   int num_sms = 0;
   int coop_factor_blocks = 0, coop_trsv_blocks = 0, coop_cg_blocks = 0, coop_ruiz_blocks = 0;
+  int coop_bfactor_blocks = 0, coop_btrsv_blocks = 0, coop_bcg_blocks = 0, coop_bruiz_blocks = 0;
 
   bool have_plan = false, have_kkt = false, have_values = false, have_factor = false;
   hykkt::SupernodalPlan sp;
@@ -115,6 +117,7 @@ struct hykkt_context {
   hykkt::DBuf<double> panel, y, src_vals, bvec, xvec;
   hykkt::DBuf<int> fac_done;
   hykkt::DBuf<unsigned> barrier;  // count, gen
+  hykkt::DBuf<unsigned> tickets;  // dynamic task counters
   hykkt::DBuf<hykkt::StatusBlock> status;
   int epoch = 0;
 
@@ -140,6 +143,16 @@ struct hykkt_context {
   struct OPtr { double *dx, *dy, *ds, *dyd; } o{};
   hykkt::DBuf<double> bvals, bouts;  // [batch][values], [batch][solution]
   long long batch = 0;
+  struct BatchBufsT {
+    int Bp = 32;
+    bool flags_init = false;
+    hykkt::DBuf<double> xs, vals, ht, hts, js, jscsr, rx, rxs, rys, d, norms, hg, rhat, maxdiag, panel, y, u, acc;
+    hykkt::DBuf<double> cgrhs, cgx, cgr, cgp, cgq, part, dxs, odx, ody, ods, odyd, delta1, relres;
+    hykkt::DBuf<int> ruiz_unconv, ruiz_active, sweeps, active, fail, running, start, flags, live;
+    hykkt::DBuf<int> fac_done, fdone, bdone;
+    hykkt::DBuf<long long> iters;
+    double* f[9] = {};
+  } bb;
   std::vector<hykkt_report_t> batch_reports;
 
   hykkt::dev::SnPlan snplan() const {
@@ -211,9 +224,17 @@ namespace {
 
 using Ctx = hykkt_context;
 
-void coop_launch(Ctx& c, const void* fn, int blocks, void* args) {
+// kb_trsv / kb_cg per-warp accumulators: 8 warps x rows x 32 systems.
+int batch_smem_rows() {
+  int r = 48;
+  if (const char* e = std::getenv("HYKKT_BATCH_SMEM_ROWS")) r = std::max(8, std::atoi(e));
+  return r;
+}
+const std::size_t kBatchSmem = 8 * static_cast<std::size_t>(batch_smem_rows()) * 32 * sizeof(double);
+
+void coop_launch(Ctx& c, const void* fn, int blocks, void* args, std::size_t smem = 0) {
   void* argv[] = {args};
-  CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), argv, 0, c.stream));
+  CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), argv, smem, c.stream));
   c.launches++;
 }
 
@@ -225,9 +246,10 @@ void check_launch(Ctx& c) {
 // Resident blocks for a cooperative persistent kernel: occupancy-limited and
 // capped at HYKKT_BLOCKS_PER_SM (default 4 -> 32 warps per SM): more
 // resident warps than that only add pollers.
-int occupancy_blocks(Ctx& c, const void* fn) {
+int occupancy_blocks(Ctx& c, const void* fn, std::size_t smem = 0) {
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+  if (smem) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
   int cap = 4;
   if (const char* e = std::getenv("HYKKT_BLOCKS_PER_SM")) cap = std::max(1, std::atoi(e));
   return std::max(1, std::min(per_sm, cap)) * c.num_sms;
@@ -245,6 +267,16 @@ void init_ctx(Ctx& c, int device) {
   c.coop_trsv_blocks = occupancy_blocks(c, (const void*)dev::k_trsv);
   c.coop_cg_blocks = occupancy_blocks(c, (const void*)dev::k_cg);
   c.coop_ruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_ruiz), 2 * c.num_sms);
+  c.coop_bfactor_blocks = occupancy_blocks(c, (const void*)dev::kb_factor);
+  c.coop_btrsv_blocks = occupancy_blocks(c, (const void*)dev::kb_trsv, kBatchSmem);
+  // batched CG: grid * 256 must be a multiple of the system stride (a power
+  // of two <= 2^16): use a power-of-two number of blocks.
+  {
+    int nb = occupancy_blocks(c, (const void*)dev::kb_cg, kBatchSmem), p2 = 1;
+    while (p2 * 2 <= nb) p2 *= 2;
+    c.coop_bcg_blocks = p2;
+  }
+  c.coop_bruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::kb_ruiz), 2 * c.num_sms);
   c.barrier.alloc(2);
   CK(cudaMemsetAsync(c.barrier.p, 0, 2 * sizeof(unsigned), c.stream));
   c.status.alloc(1);
@@ -304,6 +336,13 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   c.have_factor = false;
 }
 
+// Zeroed task counters for the next launch (one per pass).
+unsigned* fresh_tickets(Ctx& c, long long n) {
+  if (static_cast<long long>(c.tickets.n) < n) c.tickets.alloc(static_cast<std::size_t>(n));
+  CK(cudaMemsetAsync(c.tickets.p, 0, n * sizeof(unsigned), c.stream));
+  return c.tickets.p;
+}
+
 StatusBlock read_status(Ctx& c) {
   StatusBlock sb;
   CK(cudaMemcpyAsync(&sb, c.status.p, sizeof(sb), cudaMemcpyDeviceToHost, c.stream));
@@ -343,6 +382,7 @@ int factor_attempt(Ctx& c, const double* src, double delta1, double floor_abs,
   fa.floor_rel = floor_rel;
   fa.fail_col = &c.status.p->fail_col;
   fa.abort = &c.status.p->abort;
+  fa.ticket = fresh_tickets(c, 1);
   if (s.nsup > 0) coop_launch(c, (const void*)dev::k_factor, c.coop_factor_blocks, &fa);
   const StatusBlock sb = read_status(c);
   const int failed = sb.fail_col >= static_cast<int>(s.n) ? -1 : sb.fail_col;
@@ -379,6 +419,7 @@ void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, doub
   ta.rhs.b = b;
   ta.rhs.u = u;
   ta.rhs.jval = jval;
+  ta.ticket = fresh_tickets(c, 1);
   coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
 }
 
@@ -402,6 +443,7 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   a.thr = cfg.small_quadratic_threshold;
   a.max_iter = cfg.cg_max_iter;
   a.res = &c.status.p->cg;
+  a.tickets = fresh_tickets(c, cfg.cg_max_iter + 2);
   if (c.sp.nsup == 0 && c.kp.mc > 0) throw StateError("empty factor with constraints");
   coop_launch(c, (const void*)dev::k_cg, c.coop_cg_blocks, &a);
   return read_status(c).cg;
@@ -787,6 +829,9 @@ BatchLayout batch_layout(const KktPlan& k) {
   return L;
 }
 
+int pow2_at_least(long long v);
+void batch_interleave_inputs(Ctx& c);
+
 void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v) {
   if (!c.have_kkt) throw StateError("hykkt_analyze must be called first");
   if (batch <= 0) throw InvalidArgument("batch must be positive");
@@ -805,41 +850,345 @@ void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v) {
   c.bouts.alloc(static_cast<std::size_t>(batch * nout));
   c.batch = batch;
   c.batch_reports.assign(batch, hykkt_report_t{});
+  const int newBp = pow2_at_least(batch);
+  if (newBp != c.bb.Bp) c.bb.flags_init = false;
+  c.bb.Bp = newBp;
+  batch_interleave_inputs(c);
 }
 
+int pow2_at_least(long long v) {
+  int p = 32;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// Interleaved [entry][system] copies of the uploaded field-major values.
+void batch_interleave_inputs(Ctx& c) {
+  auto& bb = c.bb;
+  const BatchLayout L = batch_layout(c.kp);
+  const int B = static_cast<int>(c.batch), Bp = bb.Bp;
+  idx total = 0;
+  for (int i = 0; i < 9; ++i) total += L.sizes[i];
+  bb.vals.alloc(static_cast<std::size_t>(total) * Bp);
+  idx off_in = 0, off_out = 0;
+  for (int i = 0; i < 9; ++i) {
+    const idx n = L.sizes[i];
+    bb.f[i] = bb.vals.p + off_out * Bp;
+    if (n > 0) {
+      dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>(Bp / 32));
+      dev::kb_interleave<<<grid, 256, 0, c.stream>>>(c.bvals.p + off_in, bb.f[i], static_cast<int>(n), B, Bp);
+      check_launch(c);
+    }
+    off_in += n * B;
+    off_out += n;
+  }
+}
+
+template <typename T>
+void balloc(hykkt::DBuf<T>& buf, idx n, int Bp) { buf.alloc(static_cast<std::size_t>(std::max<idx>(n, 1)) * Bp); }
+
+// The batched device path: every phase of solve_full for all systems at once
+// (lane = system).  Per-system outcomes follow the reference exactly: Ruiz
+// sweeps, the delta1 ladder (solver.cpp:108-142) with a fresh
+// RegularizationState per system, CG stop rules, the delta2 restart.
 void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_report_t* reports) {
   if (c.batch <= 0) throw StateError("no batch uploaded");
-  const BatchLayout L = batch_layout(c.kp);
+  validate_cfg(cfg);
   const KktPlan& k = c.kp;
-  hykkt_timing_t sum{};
-  for (idx b = 0; b < c.batch; ++b) {
-    double* f[9];
-    idx off = 0;
-    for (int i = 0; i < 9; ++i) {
-      f[i] = c.bvals.p + off + b * L.sizes[i];
-      off += c.batch * L.sizes[i];
+  const SupernodalPlan& sp = c.sp;
+  auto& bb = c.bb;
+  const int B = static_cast<int>(c.batch), Bp = bb.Bp, T = Bp / 32;
+  const dev::BDims bd{B, Bp, T};
+  const dev::AsmPlan ap = c.asmplan();
+  cudaStream_t st = c.stream;
+  const long long launches0 = c.launches;
+  Events ev;
+  if (flags & HYKKT_FLAG_TIMING) ev.create();
+  const idx nx = k.nx, mc = k.mc, md = k.md;
+  // work buffers (x Bp)
+  balloc(bb.ht, k.ht.nnz(), Bp); balloc(bb.hts, k.ht.nnz(), Bp); balloc(bb.js, k.j.nnz(), Bp);
+  balloc(bb.jscsr, k.j.nnz(), Bp); balloc(bb.rx, nx, Bp); balloc(bb.rxs, nx, Bp); balloc(bb.rys, mc, Bp);
+  balloc(bb.d, nx + mc, Bp); balloc(bb.norms, nx + mc, Bp); balloc(bb.hg, k.hg.nnz(), Bp);
+  balloc(bb.rhat, nx, Bp); balloc(bb.maxdiag, 1, Bp); balloc(bb.panel, sp.panel_size, Bp);
+  balloc(bb.y, sp.n, Bp); balloc(bb.xs, sp.n, Bp); balloc(bb.u, sp.u_off.back(), Bp); balloc(bb.acc, sp.sn_rows_ptr.back(), Bp);
+  balloc(bb.cgrhs, mc, Bp); balloc(bb.cgx, mc, Bp); balloc(bb.cgr, mc, Bp); balloc(bb.cgp, mc, Bp);
+  balloc(bb.cgq, mc, Bp); balloc(bb.dxs, nx, Bp); balloc(bb.odx, nx, Bp); balloc(bb.ody, mc, Bp);
+  balloc(bb.ods, md, Bp); balloc(bb.odyd, md, Bp);
+  balloc(bb.ruiz_unconv, cfg.ruiz_max_iters + 1, Bp); bb.ruiz_active.alloc(cfg.ruiz_max_iters + 2);
+  bb.sweeps.alloc(Bp); bb.delta1.alloc(Bp); bb.active.alloc(Bp); bb.fail.alloc(Bp);
+  bb.running.alloc(Bp); bb.start.alloc(Bp); bb.flags.alloc(Bp); bb.iters.alloc(Bp); bb.relres.alloc(Bp);
+  bb.live.alloc(cfg.cg_max_iter + 2);
+  bb.fac_done.alloc(std::max<idx>(1, sp.nsup) * T); bb.fdone.alloc(std::max<idx>(1, sp.nsup) * T);
+  bb.bdone.alloc(std::max<idx>(1, sp.nsup) * T);
+  if (!bb.flags_init) {
+    CK(cudaMemsetAsync(bb.fac_done.p, 0, bb.fac_done.n * sizeof(int), st));
+    CK(cudaMemsetAsync(bb.fdone.p, 0, bb.fdone.n * sizeof(int), st));
+    CK(cudaMemsetAsync(bb.bdone.p, 0, bb.bdone.n * sizeof(int), st));
+    bb.flags_init = true;
+  }
+  dev::BVals v{bb.f[0], bb.f[1], bb.f[2], bb.f[3], bb.f[4], bb.f[5], bb.f[6], bb.f[7], bb.f[8]};
+  int* abort = &c.status.p->abort;
+  CK(cudaMemsetAsync(abort, 0, sizeof(int), st));
+  auto grid_of = [&](long long n) { return blocks_for(n * Bp); };
+
+  ev.rec(0, st);
+  // ---- assembly ----
+  dev::kb_reduce<<<grid_of(std::max<idx>(k.ht.nnz(), nx)), kThreads, 0, st>>>(ap, bd, v, bb.ht.p, bb.rx.p);
+  check_launch(c);
+  CK(cudaMemsetAsync(bb.ruiz_unconv.p, 0, bb.ruiz_unconv.n * sizeof(int), st));
+  CK(cudaMemsetAsync(bb.ruiz_active.p, 0, bb.ruiz_active.n * sizeof(int), st));
+  {
+    dev::BRuizArgs ra;
+    ra.p = ap;
+    ra.bd = bd;
+    ra.ht = bb.ht.p;
+    ra.jval = v.j;
+    ra.d = bb.d.p;
+    ra.norms = bb.norms.p;
+    ra.unconverged = bb.ruiz_unconv.p;
+    ra.active_count = bb.ruiz_active.p;
+    ra.sweeps = bb.sweeps.p;
+    ra.max_iters = static_cast<int>(cfg.ruiz_max_iters);
+    ra.tol = cfg.ruiz_tol;
+    ra.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+    ra.abort = abort;
+    coop_launch(c, (const void*)dev::kb_ruiz, c.coop_bruiz_blocks, &ra);
+  }
+  dev::kb_scale<<<grid_of(std::max<idx>({k.ht.nnz(), k.j.nnz(), nx, mc})), kThreads, 0, st>>>(
+      ap, bd, bb.d.p, bb.ht.p, v.j, bb.rx.p, v.ry, bb.hts.p, bb.js.p, bb.jscsr.p, bb.rxs.p, bb.rys.p);
+  check_launch(c);
+  CK(cudaMemsetAsync(bb.maxdiag.p, 0, Bp * sizeof(double), st));
+  dev::kb_hgamma<<<grid_of(std::max<idx>(k.hg.nnz(), nx)), kThreads, 0, st>>>(
+      ap, bd, cfg.gamma, bb.hts.p, bb.js.p, bb.rxs.p, bb.rys.p, bb.hg.p, bb.rhat.p, bb.maxdiag.p);
+  check_launch(c);
+  ev.rec(1, st);
+
+  // ---- delta1 ladder per system (solver.cpp:108-142) ----
+  std::vector<double> d1(Bp, 0.0), dmin(Bp, cfg.delta_min);
+  std::vector<int> act(Bp, 1), attempts(Bp, 0), fail(Bp, 0), failed_col(Bp, -1), ok(Bp, 0);
+  const dev::SnPlan snp = c.snplan();
+  const int nsrc = static_cast<int>(sp.src_to_panel.size());
+  for (int round = 0; round < 64; ++round) {
+    bool any = false;
+    for (int b = 0; b < Bp; ++b) any = any || act[b];
+    if (!any) break;
+    CK(cudaMemcpyAsync(bb.delta1.p, d1.data(), Bp * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(bb.active.p, act.data(), Bp * sizeof(int), cudaMemcpyHostToDevice, st));
+    dev::kb_zero_panels<<<blocks_for(sp.panel_size * Bp), kThreads, 0, st>>>(sp.panel_size, bd, bb.active.p, bb.panel.p);
+    check_launch(c);
+    if (nsrc > 0) {
+      dev::kb_scatter<<<grid_of(nsrc), kThreads, 0, st>>>(nsrc, bd, bb.hg.p, c.src_to_panel.p, c.src_row.p,
+                                                          c.src_col.p, bb.delta1.p, bb.active.p, bb.panel.p);
+      check_launch(c);
     }
-    c.v = {f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], f[8]};
-    double* o = c.bouts.p;
-    c.o = {o + b * k.nx, o + c.batch * k.nx + b * k.mc, o + c.batch * (k.nx + k.mc) + b * k.md,
-           o + c.batch * (k.nx + k.mc + k.md) + b * k.md};
-    c.have_values = true;
-    double dmin = 0.0;  // fresh RegularizationState per system
+    CK(cudaMemsetAsync(bb.fail.p, 0x7f, Bp * sizeof(int), st));
+    dev::BFactorArgs fa;
+    fa.s = snp;
+    fa.bd = bd;
+    fa.panel = bb.panel.p;
+    fa.done = bb.fac_done.p;
+    fa.epoch = ++c.epoch;
+    fa.maxdiag = bb.maxdiag.p;
+    fa.floor_rel = cfg.pivot_floor;
+    fa.floor_abs = 0.0;
+    fa.active = bb.active.p;
+    fa.fail_col = bb.fail.p;
+    fa.abort = abort;
+    fa.ticket = fresh_tickets(c, 1);
+    if (sp.nsup > 0) coop_launch(c, (const void*)dev::kb_factor, c.coop_bfactor_blocks, &fa);
+    CK(cudaMemcpyAsync(fail.data(), bb.fail.p, Bp * sizeof(int), cudaMemcpyDeviceToHost, st));
+    read_status(c);
+    for (int b = 0; b < Bp; ++b) {
+      if (!act[b]) continue;
+      ++attempts[b];
+      const bool failed = fail[b] < static_cast<int>(sp.n);
+      if (!failed) {
+        act[b] = 0;
+        ok[b] = 1;
+      } else if (d1[b] <= cfg.delta_max / 2.0) {
+        if (d1[b] == 0.0) {
+          d1[b] = dmin[b];
+        } else {
+          dmin[b] *= 2.0;
+          d1[b] = dmin[b];
+        }
+      } else {
+        act[b] = 0;
+        failed_col[b] = fail[b];
+      }
+    }
+  }
+  ev.rec(2, st);
+
+  // ---- w solve + Schur rhs ----
+  auto trsv_args = [&](const double* rb, const double* ru, double* x_out, const int* lane_on) {
+    dev::BTrsvArgs ta;
+    ta.s = snp;
+    ta.bd = bd;
+    ta.panel = bb.panel.p;
+    ta.y = bb.y.p;
+    ta.x = bb.xs.p;
+    ta.u = bb.u.p;
+    ta.acc = bb.acc.p;
+    ta.x_out = x_out;
+    ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+    ta.smem_rows = batch_smem_rows();
+    ta.fdone = bb.fdone.p;
+    ta.bdone = bb.bdone.p;
+    ta.epoch = 0;
+    ta.abort = abort;
+    ta.rb = rb;
+    ta.ru = ru;
+    ta.j_cp = c.j_cp.p;
+    ta.j_ri = c.j_ri.p;
+    ta.jval = bb.js.p;
+    ta.lane_on = lane_on;
+    return ta;
+  };
+  if (sp.nsup > 0) {
+    dev::BTrsvArgs ta = trsv_args(bb.rhat.p, nullptr, nullptr, nullptr);
+    ta.epoch = ++c.epoch;
+    ta.ticket = fresh_tickets(c, 1);
+    coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
+  }
+  if (mc > 0) {
+    dev::kb_schur_rhs<<<grid_of(mc), kThreads, 0, st>>>(static_cast<int>(mc), bd, c.jcsr_rp.p, c.jcsr_ci_perm.p,
+                                                        bb.jscsr.p, bb.xs.p, bb.rys.p, bb.cgrhs.p);
+    check_launch(c);
+  }
+  ev.rec(3, st);
+
+  // ---- CG (+ delta2 restart) ----
+  std::vector<long long> iters(Bp, 0);
+  std::vector<double> relres(Bp, 0.0), d2used(Bp, 0.0);
+  std::vector<int> cflags(Bp, 0), start(Bp, 0);
+  const long long cg0 = c.launches;
+  auto run_bcg = [&](const std::vector<int>& which, double delta2) {
+    CK(cudaMemcpyAsync(bb.start.p, which.data(), Bp * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(bb.live.p, 0, bb.live.n * sizeof(int), st));
+    dev::BCgArgs a;
+    a.tr = trsv_args(nullptr, bb.cgp.p, nullptr, bb.running.p);
+    a.mc = static_cast<int>(mc);
+    a.jcsr_rp = c.jcsr_rp.p;
+    a.jcsr_ci_perm = c.jcsr_ci_perm.p;
+    a.jcsr = bb.jscsr.p;
+    a.rhs = bb.cgrhs.p;
+    a.x = bb.cgx.p;
+    a.r = bb.cgr.p;
+    a.p = bb.cgp.p;
+    a.q = bb.cgq.p;
+    a.part = nullptr;
+    a.running = bb.running.p;
+    a.start = bb.start.p;
+    a.delta2 = delta2;
+    a.tol = cfg.cg_tol;
+    a.thr = cfg.small_quadratic_threshold;
+    a.max_iter = cfg.cg_max_iter;
+    a.epoch_base = c.epoch;
+    a.iters = bb.iters.p;
+    a.relres = bb.relres.p;
+    a.flags = bb.flags.p;
+    a.live = bb.live.p;
+    a.tickets = fresh_tickets(c, cfg.cg_max_iter + 2);
+    a.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+    const int blocks = c.coop_bcg_blocks;
+    bb.part.alloc(static_cast<std::size_t>(blocks) * kThreads);
+    a.part = bb.part.p;
+    coop_launch(c, (const void*)dev::kb_cg, blocks, &a, kBatchSmem);
+    c.epoch += static_cast<int>(std::min<long long>(cfg.cg_max_iter, 1 << 28)) + 1;
+    CK(cudaMemcpyAsync(iters.data(), bb.iters.p, Bp * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(relres.data(), bb.relres.p, Bp * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cflags.data(), bb.flags.p, Bp * sizeof(int), cudaMemcpyDeviceToHost, st));
+    read_status(c);
+  };
+  if (mc > 0) {
+    run_bcg(ok, 0.0);
+    std::vector<int> redo(Bp, 0);
+    bool any = false;
+    for (int b = 0; b < Bp; ++b) {
+      if (ok[b] && cflags[b] == 2) {
+        redo[b] = 1;
+        d2used[b] = cfg.delta2;
+        any = true;
+      }
+    }
+    if (any) run_bcg(redo, cfg.delta2);
+  } else {
+    CK(cudaMemsetAsync(bb.cgx.p, 0, bb.cgx.n * sizeof(double), st));
+    for (int b = 0; b < Bp; ++b) cflags[b] = 1;
+  }
+  const long long cg_launches = c.launches - cg0;
+  ev.rec(4, st);
+
+  // ---- dx solve, unscale, recover ----
+  if (sp.nsup > 0) {
+    dev::BTrsvArgs ta = trsv_args(bb.rhat.p, bb.cgx.p, bb.dxs.p, nullptr);
+    ta.epoch = ++c.epoch;
+    ta.ticket = fresh_tickets(c, 1);
+    coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
+  }
+  dev::kb_recover<<<grid_of(std::max<idx>({nx, mc, md})), kThreads, 0, st>>>(
+      ap, bd, c.jdcsr_rp.p, c.jdcsr_ci.p, c.jdcsr_src.p, bb.d.p, bb.dxs.p, bb.cgx.p, v, bb.odx.p, bb.ody.p,
+      bb.ods.p, bb.odyd.p);
+  check_launch(c);
+  {
+    const idx ns[4] = {nx, mc, md, md};
+    const double* src[4] = {bb.odx.p, bb.ody.p, bb.ods.p, bb.odyd.p};
+    idx off = 0;
+    for (int i = 0; i < 4; ++i) {
+      if (ns[i] > 0) {
+        dim3 grid(static_cast<unsigned>((ns[i] + 31) / 32), static_cast<unsigned>(Bp / 32));
+        dev::kb_deinterleave<<<grid, 256, 0, st>>>(src[i], c.bouts.p + off, static_cast<int>(ns[i]), B, Bp);
+        check_launch(c);
+      }
+      off += ns[i] * B;
+    }
+  }
+  ev.rec(5, st);
+  std::vector<int> sweeps(Bp, 0);
+  CK(cudaMemcpyAsync(sweeps.data(), bb.sweeps.p, Bp * sizeof(int), cudaMemcpyDeviceToHost, st));
+  read_status(c);
+
+  c.timing = hykkt_timing_t{};
+  if (ev.on) {
+    float ms[5];
+    for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev.e[i], ev.e[i + 1]));
+    c.timing.assemble_ms = ms[0];
+    c.timing.factor_ms = ms[1];
+    c.timing.solve_w_ms = ms[2];
+    c.timing.cg_ms = ms[3];
+    c.timing.solve_dx_ms = ms[4];
+    float tot;
+    CK(cudaEventElapsedTime(&tot, ev.e[0], ev.e[5]));
+    c.timing.total_ms = tot;
+  }
+  c.timing.kernel_launches = c.launches - launches0;
+  c.timing.cg_kernel_launches = cg_launches;
+
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  const idx hdiag = k.nx, hfull = 2 * (k.ht.nnz() - hdiag) + hdiag;
+  for (int b = 0; b < B; ++b) {
     hykkt_report_t r{};
-    solve_resident(c, cfg, &dmin, flags, &r);
+    r.be_4x4 = r.rr_4x4 = r.be_2x2 = r.rr_2x2 = r.be_2x2_scaled = r.rr_2x2_scaled = nan;
+    r.nnz_op = hfull + 2 * k.j.nnz() + k.nx;
+    r.nnz_fac = 2 * sp.l_nnz();
+    r.density_ratio = r.nnz_op > 0 ? static_cast<double>(r.nnz_fac) / r.nnz_op : 0.0;
+    r.rho_c = k.nx > 0 ? static_cast<double>(r.nnz_fac) / k.nx : 0.0;
+    r.ruiz_iterations = sweeps[b];
+    r.factorization_attempts = attempts[b];
+    r.delta1_final = d1[b];
+    r.failed_column = failed_col[b];
+    if (!ok[b]) {
+      r.status = 2;
+    } else {
+      r.delta2_used = d2used[b];
+      r.cg_iterations = iters[b];
+      r.cg_relative_residual = relres[b];
+      r.status = cflags[b] == 1 ? (d2used[b] > 0.0 ? 1 : 0) : 3;
+    }
     c.batch_reports[b] = r;
     if (reports) reports[b] = r;
-    sum.assemble_ms += c.timing.assemble_ms;
-    sum.factor_ms += c.timing.factor_ms;
-    sum.solve_w_ms += c.timing.solve_w_ms;
-    sum.cg_ms += c.timing.cg_ms;
-    sum.solve_dx_ms += c.timing.solve_dx_ms;
-    sum.total_ms += c.timing.total_ms;
-    sum.kernel_launches += c.timing.kernel_launches;
-    sum.cg_kernel_launches += c.timing.cg_kernel_launches;
   }
-  c.timing = sum;
-  c.have_values = false;  // c.v points into the batch; single-system values must be re-uploaded
 }
 
 void batch_download(Ctx& c, double* dx, double* ds, double* dy, double* dyd) {
@@ -1120,6 +1469,45 @@ int hykkt_chol_get_factor(hykkt_t h, int64_t* l_colptr, int64_t* l_rowidx, doubl
   });
 }
 
+// Diagnostics: one traced batched H^-1 pass over the last batch (needs a
+// solved batch); out[t] / out[2 ntask + t] = end / start ns of task t.
+int hykkt_debug_btrsv_trace(hykkt_t h, uint64_t* out) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    auto& bb = c.bb;
+    const int T = bb.Bp / 32;
+    const idx nt = c.sp.nsup * T;
+    hykkt::DBuf<unsigned long long> tr;
+    tr.alloc(4 * nt);
+    dev::BTrsvArgs ta;
+    ta.s = c.snplan();
+    ta.bd = dev::BDims{static_cast<int>(c.batch), bb.Bp, T};
+    ta.panel = bb.panel.p;
+    ta.y = bb.y.p;
+    ta.x = bb.xs.p;
+    ta.u = bb.u.p;
+    ta.acc = bb.acc.p;
+    ta.x_out = nullptr;
+    ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+    ta.smem_rows = batch_smem_rows();
+    ta.fdone = bb.fdone.p;
+    ta.bdone = bb.bdone.p;
+    ta.epoch = ++c.epoch;
+    ta.abort = &c.status.p->abort;
+    ta.rb = bb.rhat.p;
+    ta.ru = nullptr;
+    ta.j_cp = c.j_cp.p;
+    ta.j_ri = c.j_ri.p;
+    ta.jval = bb.js.p;
+    ta.lane_on = nullptr;
+    ta.trace = tr.p;
+    ta.ticket = fresh_tickets(c, 1);
+    coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
+    read_status(c);
+    CK(cudaMemcpy(out, tr.p, 4 * nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
 // Diagnostics: supernode structure (order, first column, rows, parent).
 int hykkt_debug_plan(hykkt_t h, int32_t* order, int32_t* first, int32_t* nrows, int32_t* parent) {
   return guarded([&] {
@@ -1146,6 +1534,7 @@ int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
     dev::TrsvArgs ta = trsv_args(c);
     ta.rhs.b = c.rhat.p;
     ta.trace = tr.p;
+    ta.ticket = fresh_tickets(c, 1);
     coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
     read_status(c);
     CK(cudaMemcpy(out, tr.p, 6 * ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost));

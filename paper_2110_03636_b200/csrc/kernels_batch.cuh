@@ -1,0 +1,809 @@
+// Batched HyKKT: B independent systems on one shared pattern (BASELINE
+// configs[4]).  Lane = system: every value array is interleaved
+// [entry][system] with a system stride Bp (B rounded up to 32; pad lanes
+// replicate the last system), so a warp touching one entry for 32 systems
+// issues one fully coalesced 256-byte access.  Tasks are (supernode, tile of
+// 32 systems) warp tasks on the same level-sorted sync-free schedule as the
+// single-system path; each lane runs the scalar algorithm for its system, so
+// the per-hop latency of the elimination tree is amortised over 32 systems
+// and the batch becomes bandwidth-bound.
+//
+// Arithmetic follows the single-system kernels (which restate the
+// reference: kkt_system.cpp:66-105, ruiz.cpp:26-133, solver.cpp:66-201,
+// cholesky.cpp:65-168) lane by lane; per-system outcomes (Ruiz sweeps, delta1
+// ladder, CG iterations, small quadratic) are tracked per lane.
+#pragma once
+
+#include "kernels_assemble.cuh"
+#include "kernels_solve.cuh"
+
+namespace hykkt::dev {
+
+struct BDims {
+  int B;    // real systems
+  int Bp;   // padded stride (multiple of 32)
+  int T;    // tiles = Bp / 32
+};
+
+__device__ __forceinline__ long long bidx(long long e, int Bp, int b) { return e * Bp + b; }
+
+// [system][entry] (field-major, B systems) -> [entry][system] (Bp stride).
+__global__ void kb_interleave(const double* __restrict__ in, double* __restrict__ out, int n, int B,
+                              int Bp) {
+  __shared__ double tile[32][33];
+  const int e0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  for (int j = ty; j < 32; j += 8) {
+    const int b = min(b0 + j, B - 1), e = e0 + tx;
+    tile[j][tx] = e < n ? in[(long long)b * n + e] : 0.0;
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int e = e0 + j, b = b0 + tx;
+    if (e < n) out[(long long)e * Bp + b] = tile[tx][j];
+  }
+}
+
+// [entry][system] -> [system][entry] for the first B systems.
+__global__ void kb_deinterleave(const double* __restrict__ in, double* __restrict__ out, int n, int B,
+                                int Bp) {
+  __shared__ double tile[32][33];
+  const int e0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int j = ty; j < 32; j += 8) {
+    const int e = e0 + j;
+    tile[j][tx] = e < n ? in[(long long)e * Bp + b0 + tx] : 0.0;
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int b = b0 + j, e = e0 + tx;
+    if (b < B && e < n) out[(long long)b * n + e] = tile[tx][j];
+  }
+}
+
+struct BVals {  // interleaved inputs
+  const double *h, *j, *jd, *dx, *ds, *rtx, *rs, *ry, *ryd;
+};
+
+// ---- assembly ---------------------------------------------------------------
+__global__ void kb_reduce(AsmPlan p, BDims bd, BVals v, double* __restrict__ ht, double* __restrict__ r_x) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int b = static_cast<int>(g % bd.Bp);
+  const long long t = g / bd.Bp;
+  const int Bp = bd.Bp;
+  if (t < p.n_ht) {
+    const int col = p.ht_col[t];
+    double x = (p.ht_row[t] == col) ? v.dx[bidx(col, Bp, b)] : 0.0;
+    const int hs = p.ht_hsrc[t];
+    if (hs >= 0) x = __dadd_rn(x, v.h[bidx(hs, Bp, b)]);
+    const int q0 = p.ht_pp[t], q1 = p.ht_pp[t + 1];
+    if (q1 > q0) {
+      double s = 0.0;
+      for (int q = q0; q < q1; ++q) {
+        s = __dadd_rn(s, __dmul_rn(__dmul_rn(v.ds[bidx(p.ht_pk[q], Bp, b)], v.jd[bidx(p.ht_pa[q], Bp, b)]),
+                                   v.jd[bidx(p.ht_pb[q], Bp, b)]));
+      }
+      x = __dadd_rn(x, s);
+    }
+    ht[bidx(t, Bp, b)] = x;
+  }
+  if (t < p.nx) {
+    double acc = 0.0;
+    for (int q = p.jd_cp[t]; q < p.jd_cp[t + 1]; ++q) {
+      const int k = p.jd_ri[q];
+      const double tk = __dadd_rn(__dmul_rn(v.ds[bidx(k, Bp, b)], v.ryd[bidx(k, Bp, b)]), v.rs[bidx(k, Bp, b)]);
+      acc = __dadd_rn(acc, __dmul_rn(v.jd[bidx(q, Bp, b)], tk));
+    }
+    r_x[bidx(t, Bp, b)] = __dadd_rn(acc, v.rtx[bidx(t, Bp, b)]);
+  }
+}
+
+struct BRuizArgs {
+  AsmPlan p;
+  BDims bd;
+  const double* ht;
+  const double* jval;
+  double* d;            // (n_x + m_c) x Bp
+  double* norms;        // (n_x + m_c) x Bp
+  int* unconverged;     // (max_iters + 1) x Bp, zeroed
+  int* active_count;    // max_iters + 1, zeroed
+  int* sweeps;          // Bp
+  int max_iters;
+  double tol;
+  GridBarrier bar;
+  int* abort;
+};
+
+// ruiz_scale (ruiz.cpp:76-116) for every system in lockstep; a system stops
+// updating after the sweep at which its norms converge.
+__global__ void kb_ruiz(BRuizArgs a) {
+  const int Bp = a.bd.Bp;
+  const long long nrow = (long long)(a.p.nx + a.p.mc) * Bp;
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  for (long long i = gt; i < nrow; i += gs) a.d[i] = 1.0;
+  for (long long b = gt; b < Bp; b += gs) a.sweeps[b] = a.max_iters;
+  grid_sync(a.bar, a.abort);
+  for (int it = 1; it <= a.max_iters; ++it) {
+    const int* prev = a.unconverged + (it - 1) * Bp;  // row 0 is all-unconverged by convention
+    for (long long i = gt; i < nrow; i += gs) a.norms[i] = 0.0;
+    grid_sync(a.bar, a.abort);
+    const long long nh = (long long)a.p.n_ht * Bp;
+    for (long long g = gt; g < nh; g += gs) {
+      const int b = static_cast<int>(g % Bp);
+      if (it > 1 && !ldcg_int(prev + b)) continue;
+      const long long t = g / Bp;
+      const int i = a.p.ht_row[t], j = a.p.ht_col[t];
+      const double v = __dmul_rn(__dmul_rn(fabs(a.ht[g]), ldcg(a.d + bidx(i, Bp, b))), ldcg(a.d + bidx(j, Bp, b)));
+      atomic_max_nonneg(a.norms + bidx(i, Bp, b), v);
+      if (i != j) atomic_max_nonneg(a.norms + bidx(j, Bp, b), v);
+    }
+    const long long nj = (long long)a.p.nnz_j * Bp;
+    for (long long g = gt; g < nj; g += gs) {
+      const int b = static_cast<int>(g % Bp);
+      if (it > 1 && !ldcg_int(prev + b)) continue;
+      const long long q = g / Bp;
+      const int k = a.p.j_ri[q], j = a.p.j_col[q];
+      const double v = __dmul_rn(__dmul_rn(fabs(a.jval[g]), ldcg(a.d + bidx(a.p.nx + k, Bp, b))),
+                                 ldcg(a.d + bidx(j, Bp, b)));
+      atomic_max_nonneg(a.norms + bidx(a.p.nx + k, Bp, b), v);
+      atomic_max_nonneg(a.norms + bidx(j, Bp, b), v);
+    }
+    grid_sync(a.bar, a.abort);
+    int* cur = a.unconverged + it * Bp;
+    for (long long g = gt; g < nrow; g += gs) {
+      const int b = static_cast<int>(g % Bp);
+      if (it > 1 && !ldcg_int(prev + b)) continue;
+      const double v = ldcg(a.norms + g);
+      if (v > 0.0 && fabs(v - 1.0) > a.tol) atomicOr(cur + b, 1);
+    }
+    grid_sync(a.bar, a.abort);
+    for (long long b = gt; b < Bp; b += gs) {
+      const bool was_active = it == 1 || ldcg_int(prev + b);
+      if (was_active && !ldcg_int(cur + b)) a.sweeps[b] = it;  // converged at this sweep
+      if (ldcg_int(cur + b)) atomicAdd(a.active_count + it, 1);
+    }
+    for (long long g = gt; g < nrow; g += gs) {
+      const int b = static_cast<int>(g % Bp);
+      if (!ldcg_int(cur + b)) continue;
+      const double v = ldcg(a.norms + g);
+      if (v > 0.0) a.d[g] = __ddiv_rn(ldcg(a.d + g), __dsqrt_rn(v));
+    }
+    grid_sync(a.bar, a.abort);
+    if (ldcg_int(a.active_count + it) == 0) break;
+  }
+}
+
+__global__ void kb_scale(AsmPlan p, BDims bd, const double* __restrict__ d, const double* __restrict__ ht,
+                         const double* __restrict__ jval, const double* __restrict__ r_x,
+                         const double* __restrict__ r_y, double* __restrict__ hts, double* __restrict__ js,
+                         double* __restrict__ js_csr, double* __restrict__ rxs, double* __restrict__ rys) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
+  const long long t = g / Bp;
+  if (t < p.n_ht) hts[g] = __dmul_rn(ht[g], __dmul_rn(d[bidx(p.ht_row[t], Bp, b)], d[bidx(p.ht_col[t], Bp, b)]));
+  if (t < p.nnz_j) {
+    js[g] = __dmul_rn(jval[g], __dmul_rn(d[bidx(p.nx + p.j_ri[t], Bp, b)], d[bidx(p.j_col[t], Bp, b)]));
+    const int s = p.jcsr_src[t];
+    js_csr[g] = __dmul_rn(jval[bidx(s, Bp, b)], __dmul_rn(d[bidx(p.nx + p.j_ri[s], Bp, b)], d[bidx(p.j_col[s], Bp, b)]));
+  }
+  if (t < p.nx) rxs[g] = __dmul_rn(d[g], r_x[g]);
+  if (t < p.mc) rys[g] = __dmul_rn(d[bidx(p.nx + t, Bp, b)], r_y[g]);
+}
+
+__global__ void kb_hgamma(AsmPlan p, BDims bd, double gamma, const double* __restrict__ hts,
+                          const double* __restrict__ js, const double* __restrict__ rxs,
+                          const double* __restrict__ rys, double* __restrict__ hg, double* __restrict__ rhat,
+                          double* __restrict__ maxdiag) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
+  const long long t = g / Bp;
+  if (t < p.n_hg) {
+    const int src = p.hg_src[t];
+    double v = (src >= 0) ? __dadd_rn(0.0, hts[bidx(src, Bp, b)]) : 0.0;
+    const int q0 = p.hg_pp[t], q1 = p.hg_pp[t + 1];
+    if (q1 > q0) {
+      double s = 0.0;
+      for (int q = q0; q < q1; ++q) s = __dadd_rn(s, __dmul_rn(js[bidx(p.hg_pa[q], Bp, b)], js[bidx(p.hg_pb[q], Bp, b)]));
+      v = __dadd_rn(v, __dmul_rn(gamma, s));
+    }
+    hg[g] = v;
+    if (p.hg_row[t] == p.hg_col[t]) atomic_max_nonneg(maxdiag + b, fabs(v));
+  }
+  if (t < p.nx) {
+    double acc = 0.0;
+    for (int q = p.j_cp[t]; q < p.j_cp[t + 1]; ++q) acc = __dadd_rn(acc, __dmul_rn(js[bidx(q, Bp, b)], rys[bidx(p.j_ri[q], Bp, b)]));
+    rhat[g] = __dadd_rn(rxs[g], __dmul_rn(gamma, acc));
+  }
+}
+
+// H_delta slots of the systems still on the ladder -> their panels.
+__global__ void kb_scatter(int nsrc, BDims bd, const double* __restrict__ src, const int* __restrict__ to_panel,
+                           const int* __restrict__ srow, const int* __restrict__ scol,
+                           const double* __restrict__ delta1, const int* __restrict__ active,
+                           double* __restrict__ panel) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
+  const long long t = g / Bp;
+  if (t >= nsrc || !active[b]) return;
+  double v = src[g];
+  const double d1 = delta1[b];
+  if (d1 != 0.0 && srow[t] == scol[t]) v = __dadd_rn(v, d1);
+  panel[bidx(to_panel[t], Bp, b)] = v;
+}
+
+__global__ void kb_zero_panels(long long nslots, BDims bd, const int* __restrict__ active, double* __restrict__ panel) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g < nslots * bd.Bp && active[g % bd.Bp]) panel[g] = 0.0;
+}
+
+// ---- factorization ----------------------------------------------------------
+struct BFactorArgs {
+  SnPlan s;
+  BDims bd;
+  double* panel;        // panel_size x Bp
+  int* done;            // nsup x T
+  int epoch;
+  const double* maxdiag;
+  double floor_rel;
+  double floor_abs;
+  const int* active;    // Bp
+  int* fail_col;        // Bp
+  int* abort;
+  unsigned* ticket;
+};
+
+// Per-lane dense work is written as blocks of independent loads followed by
+// the dependent arithmetic and stores: the compiler cannot move loads across
+// stores to possibly-aliasing global addresses, so without the explicit
+// blocking every step of a lane's sequential loop would pay an L2 round trip.
+constexpr int kIlp = 8;
+
+__device__ void bfactor_task(const BFactorArgs& a, int sn, int tile, int lane) {
+  const SnPlan& s = a.s;
+  const int Bp = a.bd.Bp, T = a.bd.T, b = tile * 32 + lane;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const int* R = s.rows + s.rows_ptr[sn];
+  for (int c = s.child_ptr[sn] + lane; c < s.child_ptr[sn + 1]; c += 32) {
+    wait_flag(a.done + s.child[c] * T + tile, a.epoch, a.abort);
+  }
+  __syncwarp();
+  fence_gpu();
+  // Only systems still on the ladder recompute (the others keep their L).
+  const bool act = a.active[b] != 0;
+  if (act) {
+    double* P = a.panel + (long long)s.off[sn] * Bp + b;
+    const double floor_v = fmax(a.maxdiag ? a.floor_rel * a.maxdiag[b] : a.floor_abs, 0.0);
+    for (int u = s.upd_ptr[sn]; u < s.upd_ptr[sn + 1]; ++u) {
+      const int d = s.upd_d[u], o = s.upd_off[u], cnt = s.upd_cnt[u];
+      const int nrd = s.nrows[d], wd = s.first[d + 1] - s.first[d];
+      const double* Pd = a.panel + (long long)s.off[d] * Bp + b;
+      const int* Rd = s.rows + s.rows_ptr[d];
+      const int m = nrd - o;
+      for (int jj = 0; jj < cnt; ++jj) {
+        const int cc = __ldg(Rd + o + jj) - f;
+        for (int k0 = 0; k0 < wd; k0 += 4) {
+          const int kn = min(4, wd - k0);
+          double lj[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) lj[k] = k < kn ? ldcg(Pd + (long long)((k0 + k) * nrd + o + jj) * Bp) : 0.0;
+          for (int i0 = jj; i0 < m; i0 += kIlp) {
+            double dot[kIlp];
+            int pos[kIlp];
+#pragma unroll
+            for (int t = 0; t < kIlp; ++t) {
+              const int ii = i0 + t;
+              dot[t] = 0.0;
+              pos[t] = -1;
+              if (ii < m) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  if (k < kn) dot[t] = fma(ldcg(Pd + (long long)((k0 + k) * nrd + o + ii) * Bp), lj[k], dot[t]);
+                }
+                const int r = __ldg(Rd + o + ii);
+                pos[t] = (ii < cnt) ? (r - f) : find_row(R, w, nr, r);
+              }
+            }
+            double cur[kIlp];
+#pragma unroll
+            for (int t = 0; t < kIlp; ++t) cur[t] = pos[t] >= 0 ? P[(long long)(cc * nr + pos[t]) * Bp] : 0.0;
+#pragma unroll
+            for (int t = 0; t < kIlp; ++t) {
+              if (pos[t] >= 0) P[(long long)(cc * nr + pos[t]) * Bp] = cur[t] - dot[t];
+            }
+          }
+        }
+      }
+    }
+    bool failed = false;
+    for (int k = 0; k < w; ++k) {
+      double* Pk = P + (long long)k * nr * Bp;
+      const double pivot = Pk[(long long)k * Bp];
+      if (!(pivot > floor_v) && !failed) {
+        failed = true;
+        atomicMin(a.fail_col + b, f + k);
+      }
+      const double dk = sqrt(pivot);
+      Pk[(long long)k * Bp] = dk;
+      for (int r0 = k + 1; r0 < nr; r0 += kIlp) {
+        double v[kIlp];
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) v[t] = r0 + t < nr ? Pk[(long long)(r0 + t) * Bp] : 0.0;
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+          if (r0 + t < nr) Pk[(long long)(r0 + t) * Bp] = v[t] / dk;
+        }
+      }
+      for (int c = k + 1; c < w; ++c) {
+        const double lck = Pk[(long long)c * Bp];
+        double* Pc = P + (long long)c * nr * Bp;
+        for (int r0 = c; r0 < nr; r0 += kIlp) {
+          double lk[kIlp], pc[kIlp];
+#pragma unroll
+          for (int t = 0; t < kIlp; ++t) {
+            lk[t] = r0 + t < nr ? Pk[(long long)(r0 + t) * Bp] : 0.0;
+            pc[t] = r0 + t < nr ? Pc[(long long)(r0 + t) * Bp] : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < kIlp; ++t) {
+            if (r0 + t < nr) Pc[(long long)(r0 + t) * Bp] = fma(-lk[t], lck, pc[t]);
+          }
+        }
+      }
+    }
+  }
+  warp_publish(a.done + sn * T + tile, a.epoch, lane);
+}
+
+__global__ void __launch_bounds__(256) kb_factor(BFactorArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int T = a.bd.T;
+  const long long ntask = (long long)a.s.nsup * T;
+  (void)gw;
+  (void)nw;
+  for (long long t = grab_task(a.ticket, lane); t < ntask; t = grab_task(a.ticket, lane)) {
+    bfactor_task(a, a.s.order[t / T], static_cast<int>(t % T), lane);
+  }
+}
+
+// ---- triangular solves ------------------------------------------------------
+struct BTrsvArgs {
+  SnPlan s;
+  BDims bd;
+  const double* panel;
+  double* y;         // n x Bp forward result (permuted)
+  double* x;         // n x Bp backward result (permuted)
+  double* u;         // u_size x Bp
+  double* acc;       // rows_ptr[nsup] x Bp scratch
+  double* x_out;     // original order n x Bp, or null
+  int* fdone;        // nsup x T
+  int* bdone;        // nsup x T
+  int epoch;
+  int* abort;
+  // rhs: b[perm i] (- or +) J^T u
+  const double* rb;  // n x Bp original order, or null
+  const double* ru;  // m_c x Bp, or null
+  const int* j_cp;
+  const int* j_ri;
+  const double* jval;  // nnz(J) x Bp
+  const int* lane_on;  // Bp: 0 = system finished, skip its arithmetic (or null)
+  GridBarrier bar;
+  int smem_rows;       // per-warp shared accumulator rows (dynamic smem = 8 * rows * 256 B)
+  unsigned* ticket;    // task counter of this pass (zero on entry)
+  unsigned long long* trace = nullptr;  // diagnostics
+};
+
+__device__ __forceinline__ double brhs(const BTrsvArgs& a, int i, int b) {
+  const int Bp = a.bd.Bp;
+  const int o = a.s.perm[i];
+  double bi = a.rb ? a.rb[bidx(o, Bp, b)] : 0.0;
+  if (a.ru) {
+    double t = 0.0;
+    for (int q = a.j_cp[o]; q < a.j_cp[o + 1]; ++q) {
+      t = __dadd_rn(t, __dmul_rn(a.jval[bidx(q, Bp, b)], ldcg(a.ru + bidx(a.j_ri[q], Bp, b))));
+    }
+    bi = a.rb ? __dsub_rn(bi, t) : t;
+  }
+  return bi;
+}
+
+// Per-warp shared-memory accumulator for supernodes with <= 32 structure
+// rows: A[q][lane].  Larger ones use the global scratch (stride Bp).
+constexpr int kSmemRows = 32;
+// Dense parts are processed in chunks of kC columns held in registers, so a
+// lane's global read-modify-writes happen once per chunk, not per column.
+constexpr int kC = 8;
+
+// Forward task (multifrontal, lane = system): extend-add the children's
+// update vectors, chunked triangular solve of the diagonal block, rank-kC
+// updates of the rows below, publish y and u.  Values are the
+// synchronisation: every value read from another task is checked against
+// kUnset (and polled if not there yet), so no flags or fences are needed.
+__device__ __forceinline__ void bfwd_core(const BTrsvArgs& a, int sn, int b, double* A, long long as) {
+  const SnPlan& s = a.s;
+  const int Bp = a.bd.Bp;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  // Wait: one coalesced poll per child on its last update entry for this
+  // lane's system; the loads below re-check every value anyway.
+  for (int c = s.child_ptr[sn]; c < s.child_ptr[sn + 1]; ++c) {
+    const int ch = s.child[c];
+    poll_value(a.u + (long long)(s.u_off[ch + 1] - 1) * Bp + b, a.abort);
+  }
+  for (int c = s.child_ptr[sn]; c < s.child_ptr[sn + 1]; ++c) {
+    const int ch = s.child[c];
+    const int m = s.nrows[ch] - (s.first[ch + 1] - s.first[ch]);
+    const double* uc = a.u + (long long)s.u_off[ch] * Bp + b;
+    const int* rel = s.relind + s.u_off[ch];
+    for (int t0 = 0; t0 < m; t0 += kIlp) {
+      int q[kIlp];
+      double v[kIlp], cur[kIlp];
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) q[t] = t0 + t < m ? __ldg(rel + t0 + t) : -1;
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) v[t] = q[t] >= 0 ? ldcg(uc + (long long)(t0 + t) * Bp) : 0.0;
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) cur[t] = q[t] >= 0 ? A[q[t] * as] : 0.0;
+      bool bad = false;
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) bad |= (q[t] >= 0) && __double_as_longlong(v[t]) == kUnset;
+      if (bad) {
+#pragma unroll
+        for (int t = 0; t < kIlp; ++t) {
+          if (q[t] >= 0) v[t] = load_ready(uc + (long long)(t0 + t) * Bp, a.abort);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) {
+        if (q[t] >= 0) A[q[t] * as] = cur[t] + ((q[t] < w) ? -v[t] : v[t]);
+      }
+    }
+  }
+  const double* P = a.panel + (long long)s.off[sn] * Bp + b;
+  for (int cb = 0; cb < w; cb += kC) {
+    const int cw = min(kC, w - cb);
+    double yv[kC], ad[kC];
+#pragma unroll
+    for (int k = 0; k < kC; ++k) ad[k] = k < cw ? A[(cb + k) * as] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kC; ++k) {
+      yv[k] = 0.0;
+      if (k < cw) {
+        double acc = ad[k];
+#pragma unroll
+        for (int j = 0; j < kC; ++j) {
+          if (j < k) acc = fma(-__ldg(P + (long long)((cb + j) * nr + cb + k) * Bp), yv[j], acc);
+        }
+        yv[k] = acc / __ldg(P + (long long)((cb + k) * nr + cb + k) * Bp);
+        stcg(a.y + bidx(f + cb + k, Bp, b), yv[k]);
+      }
+    }
+    for (int q0 = cb + cw; q0 < nr; q0 += kIlp) {
+      double av[kIlp];
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) av[t] = q0 + t < nr ? A[(q0 + t) * as] : 0.0;
+#pragma unroll
+      for (int k = 0; k < kC; ++k) {
+        if (k < cw) {
+#pragma unroll
+          for (int t = 0; t < kIlp; ++t) {
+            const int q = q0 + t;
+            if (q < nr) {
+              const double l = __ldg(P + (long long)((cb + k) * nr + q) * Bp);
+              av[t] = (q < w) ? fma(-l, yv[k], av[t]) : fma(l, yv[k], av[t]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) {
+        if (q0 + t < nr) A[(q0 + t) * as] = av[t];
+      }
+    }
+  }
+  double* U = a.u + (long long)s.u_off[sn] * Bp + b;
+  for (int q0 = w; q0 < nr; q0 += kIlp) {
+    double v[kIlp];
+#pragma unroll
+    for (int t = 0; t < kIlp; ++t) v[t] = q0 + t < nr ? A[(q0 + t) * as] : 0.0;
+#pragma unroll
+    for (int t = 0; t < kIlp; ++t) {
+      if (q0 + t < nr) stcg(U + (long long)(q0 + t - w) * Bp, v[t]);
+    }
+  }
+}
+
+__device__ void bfwd_task(const BTrsvArgs& a, int sn, int tile, int lane, double* smem_warp) {
+  const SnPlan& s = a.s;
+  const int Bp = a.bd.Bp, b = tile * 32 + lane;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  if (a.lane_on && !a.lane_on[b]) return;
+  const bool small = nr <= a.smem_rows;
+  if (small) {
+    double* A = smem_warp + lane;  // shared: the compiler keeps it in the .shared window
+    for (int q = 0; q < nr; ++q) A[q * 32] = q < w ? brhs(a, f + q, b) : 0.0;
+    bfwd_core(a, sn, b, A, 32);
+  } else {
+    double* A = a.acc + (long long)s.rows_ptr[sn] * Bp + b;
+    for (int q = 0; q < nr; ++q) A[(long long)q * Bp] = q < w ? brhs(a, f + q, b) : 0.0;
+    bfwd_core(a, sn, b, A, Bp);
+  }
+}
+
+// Backward task: wait for the parent's first column (it is published last),
+// then chunked from the last chunk: partial sums over the rows below the
+// chunk (x values checked), backward triangular solve in registers.
+__device__ void bbwd_task(const BTrsvArgs& a, int sn, int tile, int lane) {
+  const SnPlan& s = a.s;
+  const int Bp = a.bd.Bp, b = tile * 32 + lane;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const int* R = s.rows + s.rows_ptr[sn];
+  if (a.lane_on && !a.lane_on[b]) return;
+  const int par = s.parent[sn];
+  if (par >= 0) poll_value(a.x + bidx(s.first[par], Bp, b), a.abort);
+  const double* P = a.panel + (long long)s.off[sn] * Bp + b;
+  const int nchunks = (w + kC - 1) / kC;
+  for (int ci = nchunks - 1; ci >= 0; --ci) {
+    const int cb = ci * kC, cw = min(kC, w - cb);
+    double S[kC];
+#pragma unroll
+    for (int k = 0; k < kC; ++k) S[k] = 0.0;
+    for (int r0 = cb + cw; r0 < nr; r0 += kIlp) {
+      double xv[kIlp];
+#pragma unroll
+      for (int t = 0; t < kIlp; ++t) xv[t] = r0 + t < nr ? load_ready(a.x + bidx(__ldg(R + r0 + t), Bp, b), a.abort) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kC; ++k) {
+        if (k < cw) {
+#pragma unroll
+          for (int t = 0; t < kIlp; ++t) {
+            if (r0 + t < nr) S[k] = fma(__ldg(P + (long long)((cb + k) * nr + r0 + t) * Bp), xv[t], S[k]);
+          }
+        }
+      }
+    }
+    double xc[kC];
+#pragma unroll
+    for (int k = kC - 1; k >= 0; --k) {
+      xc[k] = 0.0;
+      if (k < cw) {
+        double acc = load_ready(a.y + bidx(f + cb + k, Bp, b), a.abort) - S[k];
+#pragma unroll
+        for (int j = 0; j < kC; ++j) {
+          if (j > k && j < cw) acc = fma(-__ldg(P + (long long)((cb + k) * nr + cb + j) * Bp), xc[j], acc);
+        }
+        xc[k] = acc / __ldg(P + (long long)((cb + k) * nr + cb + k) * Bp);
+        stcg(a.x + bidx(f + cb + k, Bp, b), xc[k]);
+        if (a.x_out) a.x_out[bidx(s.perm[f + cb + k], Bp, b)] = xc[k];
+      }
+    }
+  }
+}
+
+extern __shared__ double bsmem[];  // 8 warps x kSmemRows x 32 doubles
+
+__device__ __forceinline__ void brearm(const BTrsvArgs& a) {
+  const double u = __longlong_as_double(kUnset);
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  const long long ny = (long long)a.s.n * a.bd.Bp, nu = (long long)a.s.u_size * a.bd.Bp;
+  for (long long i = gt; i < ny; i += gs) {
+    a.y[i] = u;
+    a.x[i] = u;
+  }
+  for (long long i = gt; i < nu; i += gs) a.u[i] = u;
+}
+
+// One forward + backward pass; y, x, u must hold kUnset on entry.
+__device__ __forceinline__ void btrsv_pass(const BTrsvArgs& a) {
+  const int lane = threadIdx.x & 31;
+  double* smem_warp = bsmem + (threadIdx.x >> 5) * a.smem_rows * 32;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int T = a.bd.T;
+  const long long ns = (long long)a.s.nsup * T;
+  (void)gw;
+  (void)nw;
+  for (long long t = grab_task(a.ticket, lane); t < 2 * ns; t = grab_task(a.ticket, lane)) {
+    if (a.trace && lane == 0) a.trace[2 * ns + t] = global_ns();
+    if (t < ns) bfwd_task(a, a.s.order[t / T], static_cast<int>(t % T), lane, smem_warp);
+    else {
+      const long long tb = 2 * ns - 1 - t;
+      bbwd_task(a, a.s.order[tb / T], static_cast<int>(tb % T), lane);
+    }
+    __syncwarp();
+    if (a.trace && lane == 0) a.trace[t] = global_ns();
+  }
+}
+
+__global__ void __launch_bounds__(256) kb_trsv(BTrsvArgs a) {
+  brearm(a);
+  grid_sync(a.bar, a.abort);
+  btrsv_pass(a);
+}
+
+// Schur rhs J w - r_y per system (w = y after the pass, permuted).
+__global__ void kb_schur_rhs(int mc, BDims bd, const int* rp, const int* ci_perm, const double* jcsr,
+                             const double* y, const double* r_y, double* rhs) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
+  const long long k = g / Bp;
+  if (k >= mc) return;
+  double acc = 0.0;
+  for (int e = rp[k]; e < rp[k + 1]; ++e) {
+    const double t = y[bidx(ci_perm[e], Bp, b)];
+    if (t == 0.0) continue;
+    acc = __dadd_rn(acc, __dmul_rn(jcsr[bidx(e, Bp, b)], t));
+  }
+  rhs[g] = __dsub_rn(acc, r_y[g]);
+}
+
+// ---- batched CG ---------------------------------------------------------------
+struct BCgArgs {
+  BTrsvArgs tr;       // ru = p, lane_on = running
+  int mc;
+  const int* jcsr_rp;
+  const int* jcsr_ci_perm;
+  const double* jcsr;  // nnz x Bp
+  const double* rhs;   // mc x Bp
+  double* x;
+  double* r;
+  double* p;
+  double* q;
+  double* part;        // gridsize doubles (per-thread partials)
+  int* running;        // Bp: 1 while the system iterates (also tr.lane_on)
+  const int* start;    // Bp: systems to run in this launch
+  double delta2;
+  double tol;
+  double thr;
+  long long max_iter;
+  int epoch_base;
+  long long* iters;    // Bp
+  double* relres;      // Bp
+  int* flags;          // Bp: 1 converged, 2 small quadratic
+  int* live;           // max_iter + 2 counters, zeroed
+  unsigned* tickets;   // max_iter + 2 task counters, zeroed
+  GridBarrier bar;
+};
+
+// Per-system reduction: thread g holds a partial for system g % Bp; the
+// grid size is a multiple of Bp, so every thread's systems are fixed.
+__device__ __forceinline__ double bsum(const BCgArgs& a, double v) {
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  a.part[gt] = v;
+  grid_sync(a.bar, a.tr.abort);
+  const int Bp = a.tr.bd.Bp;
+  double s = 0.0;
+  for (long long j = gt % Bp; j < gs; j += Bp) s += ldcg(a.part + j);
+  grid_sync(a.bar, a.tr.abort);  // partials may be overwritten after this
+  return s;
+}
+
+__global__ void __launch_bounds__(256) kb_cg(BCgArgs a) {
+  const int Bp = a.tr.bd.Bp;
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  const int b = static_cast<int>(gt % Bp);
+  const long long mcB = (long long)a.mc * Bp;
+  const bool mine = a.start[b] != 0;
+  brearm(a.tr);
+  double ss = 0.0;
+  for (long long g = gt; g < mcB; g += gs) {
+    if (!mine) continue;
+    const double v = a.rhs[g];
+    a.x[g] = 0.0;
+    a.r[g] = v;
+    stcg(a.p + g, v);
+    ss = fma(v, v, ss);
+  }
+  const double rhs_norm = sqrt(bsum(a, ss));
+  bool run = mine && rhs_norm != 0.0;
+  if (gt < Bp) {
+    a.running[b] = run ? 1 : 0;
+    if (mine && !run) {
+      a.iters[b] = 0;
+      a.relres[b] = 0.0;
+      a.flags[b] = 1;
+    }
+  }
+  double rho = rhs_norm * rhs_norm, r_norm = rhs_norm;
+  grid_sync(a.bar, a.tr.abort);
+  BTrsvArgs tr = a.tr;
+  for (long long it = 1; it <= a.max_iter; ++it) {
+    // any system still running?
+    if (gt == 0) a.live[it] = 0;
+    grid_sync(a.bar, a.tr.abort);
+    if (gt < Bp && run) atomicAdd(a.live + it, 1);
+    grid_sync(a.bar, a.tr.abort);
+    if (ld_relaxed(a.live + it) == 0 || ld_relaxed(a.tr.abort)) break;
+    tr.epoch = a.epoch_base + static_cast<int>(it);
+    tr.ticket = a.tickets + it;
+    btrsv_pass(tr);
+    grid_sync(a.bar, a.tr.abort);
+    double pq = 0.0, pp = 0.0;
+    for (long long g = gt; g < mcB; g += gs) {
+      if (!run) continue;
+      const long long k = g / Bp;
+      double qk = 0.0;
+      for (int e = a.jcsr_rp[k]; e < a.jcsr_rp[k + 1]; ++e) {
+        const double t = ldcg(tr.x + bidx(a.jcsr_ci_perm[e], Bp, b));
+        if (t == 0.0) continue;
+        qk = __dadd_rn(qk, __dmul_rn(a.jcsr[bidx(e, Bp, b)], t));
+      }
+      const double pk = ldcg(a.p + g);
+      if (a.delta2 != 0.0) qk = __dadd_rn(qk, __dmul_rn(a.delta2, pk));
+      a.q[g] = qk;
+      pq = fma(pk, qk, pq);
+      pp = fma(pk, pk, pp);
+    }
+    const double curvature = bsum(a, pq);
+    const double p_norm2 = bsum(a, pp);
+    brearm(tr);  // x no longer needed this iteration: re-arm for the next pass
+    bool stop_small = run && curvature <= a.thr * p_norm2;
+    const double alpha = rho / curvature;
+    double rr = 0.0;
+    for (long long g = gt; g < mcB; g += gs) {
+      if (!run || stop_small) continue;
+      a.x[g] = __dadd_rn(a.x[g], __dmul_rn(alpha, ldcg(a.p + g)));
+      const double rk = __dsub_rn(a.r[g], __dmul_rn(alpha, a.q[g]));
+      a.r[g] = rk;
+      rr = fma(rk, rk, rr);
+    }
+    const double rn = sqrt(bsum(a, rr));
+    if (stop_small) {
+      if (gt < Bp) {
+        a.iters[b] = it - 1;
+        a.relres[b] = r_norm / rhs_norm;
+        a.flags[b] = 2;
+      }
+      run = false;
+    } else if (run) {
+      r_norm = rn;
+      const double relres = r_norm / rhs_norm;
+      if (relres <= a.tol || it == a.max_iter) {
+        if (gt < Bp) {
+          a.iters[b] = it;
+          a.relres[b] = relres;
+          a.flags[b] = relres <= a.tol ? 1 : 0;
+        }
+        run = false;
+      } else {
+        const double rho_next = r_norm * r_norm;
+        const double beta = rho_next / rho;
+        rho = rho_next;
+        for (long long g = gt; g < mcB; g += gs) stcg(a.p + g, __dadd_rn(a.r[g], __dmul_rn(beta, ldcg(a.p + g))));
+      }
+    }
+    if (gt < Bp) a.running[b] = run ? 1 : 0;
+    grid_sync(a.bar, a.tr.abort);
+  }
+}
+
+// unscale + recover per system (ruiz.cpp:118-133, kkt_system.cpp:89-105)
+__global__ void kb_recover(AsmPlan p, BDims bd, const int* __restrict__ jd_rp, const int* __restrict__ jd_ci,
+                           const int* __restrict__ jd_src, const double* __restrict__ d,
+                           const double* __restrict__ dx_s, const double* __restrict__ dy_s, BVals v,
+                           double* __restrict__ dx, double* __restrict__ dy, double* __restrict__ ds,
+                           double* __restrict__ dyd) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
+  const long long t = g / Bp;
+  if (t < p.nx) dx[g] = __dmul_rn(d[g], dx_s[g]);
+  if (t < p.mc) dy[g] = __dmul_rn(d[bidx(p.nx + t, Bp, b)], dy_s[g]);
+  if (t < p.md) {
+    double acc = 0.0;
+    for (int q = jd_rp[t]; q < jd_rp[t + 1]; ++q) {
+      const int c = jd_ci[q];
+      const double xc = __dmul_rn(d[bidx(c, Bp, b)], dx_s[bidx(c, Bp, b)]);
+      if (xc == 0.0) continue;
+      acc = __dadd_rn(acc, __dmul_rn(v.jd[bidx(jd_src[q], Bp, b)], xc));
+    }
+    const double s = __dsub_rn(acc, v.ryd[g]);
+    ds[g] = s;
+    dyd[g] = __dsub_rn(__dmul_rn(v.ds[g], s), v.rs[g]);
+  }
+}
+
+}  // namespace hykkt::dev

@@ -62,6 +62,7 @@ struct FactorArgs {
   double floor_rel;
   int* fail_col;
   int* abort;
+  unsigned* ticket;
 };
 
 __device__ __forceinline__ int find_row(const int* rows, int lo, int hi, int r) {
@@ -138,7 +139,11 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs a) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const double floor_v = fmax(a.maxdiag ? a.floor_rel * *a.maxdiag : a.floor_abs, 0.0);
-  for (int t = gw; t < a.s.nsup; t += nw) factor_task(a, a.s.order[t], lane, floor_v);
+  (void)gw;
+  (void)nw;
+  for (long long t = grab_task(a.ticket, lane); t < a.s.nsup; t = grab_task(a.ticket, lane)) {
+    factor_task(a, a.s.order[t], lane, floor_v);
+  }
 }
 
 }  // namespace hykkt::dev

@@ -73,6 +73,7 @@ struct TrsvArgs {
   int* abort;
   SolveRhs rhs;
   GridBarrier bar;
+  unsigned* ticket;           // task counter of this pass (zero on entry)
   unsigned long long* trace;  // diagnostics: per-task end / start times (ns)
 };
 
@@ -340,7 +341,9 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int ns = a.s.nsup;
-  for (int t = gw; t < 2 * ns; t += nw) {
+  (void)gw;
+  (void)nw;
+  for (long long t = grab_task(a.ticket, lane); t < 2 * ns; t = grab_task(a.ticket, lane)) {
     if (a.trace && lane == 0) a.trace[2 * ns + t] = global_ns();
     if (t < ns) fwd_task(a, a.s.order[t], lane, t);
     else bwd_task(a, a.s.order[2 * ns - 1 - t], lane, t);
@@ -413,6 +416,7 @@ struct CgArgs {
   double thr;
   long long max_iter;
   CgResultDev* res;
+  unsigned* tickets;  // max_iter + 2 task counters, zeroed
 };
 
 // Deterministic all-blocks reduction of partials[b * 4 + slot].
@@ -448,8 +452,9 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
   }
   double rho = rhs_norm * rhs_norm;
   double r_norm = rhs_norm;
-  const TrsvArgs& tr = a.tr;
+  TrsvArgs tr = a.tr;
   for (long long it = 1; it <= a.max_iter; ++it) {
+    tr.ticket = a.tickets + it;
     trsv_pass(tr);
     grid_sync(bar, abort);
     double pq = 0.0, pp = 0.0;
