@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -386,6 +387,7 @@ int factor_attempt(Ctx& c, const double* src, double delta1, double floor_abs,
   if (s.nsup > 0) coop_launch(c, (const void*)dev::k_factor, c.coop_factor_blocks, &fa);
   const StatusBlock sb = read_status(c);
   const int failed = sb.fail_col >= static_cast<int>(s.n) ? -1 : sb.fail_col;
+  if (std::getenv("HYKKT_DEBUG")) std::fprintf(stderr, "[hykkt] factor attempt delta1=%g failed=%d\n", delta1, failed);
   return failed;
 }
 

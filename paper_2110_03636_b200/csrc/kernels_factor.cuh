@@ -79,14 +79,13 @@ __device__ void factor_task(const FactorArgs& a, int sn, int lane, double floor_
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   double* P = a.panel + s.off[sn];
   const int* R = s.rows + s.rows_ptr[sn];
-  bool ok = ld_relaxed(a.fail_col) >= f;
-  if (ok) {
-    for (int c = s.child_ptr[sn] + lane; c < s.child_ptr[sn + 1]; c += 32) {
-      if (!wait_flag(a.done + s.child[c], a.epoch, a.abort)) break;
-    }
-    __syncwarp();
-    ok = ld_relaxed(a.fail_col) >= f && !ld_relaxed(a.abort);
+  for (int c = s.child_ptr[sn] + lane; c < s.child_ptr[sn + 1]; c += 32) {
+    if (!wait_flag(a.done + s.child[c], a.epoch, a.abort)) break;
   }
+  __syncwarp();
+  // Past a recorded failure the result cannot change the reported column;
+  // such supernodes still publish (nobody waits forever) but skip the work.
+  const bool ok = __shfl_sync(0xffffffffu, ld_relaxed(a.fail_col), 0) >= f;
   if (ok) {
     // Pull updates from descendants, ascending d.
     for (int u = s.upd_ptr[sn]; u < s.upd_ptr[sn + 1]; ++u) {

@@ -136,6 +136,29 @@ class NotSpdFailure:
     pivot: float
 
 
+def check_dims(sys: BlockKkt4x4) -> None:
+    """BlockKkt4x4::validate (kkt_system.cpp:33-54), dimension part."""
+    nx, mc, md = sys.n_x, sys.m_c, sys.m_d
+    bad = None
+    if sys.h.nrows != nx:
+        bad = "H must be square"
+    elif sys.j.ncols != nx:
+        bad = "J column count must be n_x"
+    elif sys.j_d.ncols != nx:
+        bad = "J_d column count must be n_x"
+    elif len(sys.d_x) != nx or len(sys.r_tilde_x) != nx:
+        bad = "D_x and r_tilde_x must have length n_x"
+    elif len(sys.d_s) != md or len(sys.r_s) != md or len(sys.r_yd) != md:
+        bad = "D_s, r_s, r_yd must have length m_d"
+    elif len(sys.r_y) != mc:
+        bad = "r_y must have length m_c"
+    elif (np.asarray(sys.d_x) < 0).any() or (np.asarray(sys.d_s) < 0).any() or not (
+            np.isfinite(sys.d_x).all() and np.isfinite(sys.d_s).all()):
+        bad = "D_x and D_s must be nonnegative and finite"
+    if bad:
+        raise _lib.InvalidMatrixError(-1, bad)
+
+
 class Device:
     """One libhykkt handle: a device, a stream and one analysed pattern."""
 
@@ -162,6 +185,7 @@ class Device:
     # ---- analysis ----------------------------------------------------------
     def analyze(self, sys: BlockKkt4x4, perm=None) -> None:
         """Per-pattern half of solve_reduced (solver.cpp:230-235), once."""
+        check_dims(sys)
         L = _lib.lib()
         a = [i64(x) for x in (sys.h.colptr, sys.h.rowidx, sys.j.colptr, sys.j.rowidx,
                               sys.j_d.colptr, sys.j_d.rowidx)]
@@ -222,6 +246,7 @@ class Device:
         """hkkt::solve_full (solver.cpp:295-328) with this handle's symbolic
         analysis (analysed on first use, like a null `shared`)."""
         cfg = cfg or SolverConfig()
+        check_dims(sys)
         created = False
         if self._pattern is None or not self._pattern.same_pattern_as(sys):
             self.analyze(sys)
@@ -320,6 +345,7 @@ class CholeskyFactor:
 
 def host_analyze(sys: BlockKkt4x4, perm=None):
     """Host-only symbolic analysis (no GPU): returns (stats dict, ordering)."""
+    check_dims(sys)
     a = [i64(x) for x in (sys.h.colptr, sys.h.rowidx, sys.j.colptr, sys.j.rowidx,
                           sys.j_d.colptr, sys.j_d.rowidx)]
     p = None if perm is None else i64(perm)
