@@ -152,6 +152,11 @@ struct hykkt_context {
     hykkt::DBuf<int> ruiz_unconv, ruiz_active, sweeps, active, fail, running, start, flags, live;
     hykkt::DBuf<int> fac_done, fdone, bdone;
     hykkt::DBuf<long long> iters;
+    // CTA job list of the batched solve (rebuilt when the tile count changes)
+    hykkt::DBuf<int> job_ptr, job_items, fjob_ptr, fjob_items, mode, slot_sn, wdone;
+    hykkt::DBuf<unsigned char> job_kind, fjob_kind;
+    int jobs_T = -1, njobs = 0, nfjobs = 0;
+    long long nwide = 0;
     double* f[9] = {};
   } bb;
   std::vector<hykkt_report_t> batch_reports;
@@ -233,6 +238,14 @@ int batch_smem_rows() {
 }
 const std::size_t kBatchSmem = 8 * static_cast<std::size_t>(batch_smem_rows()) * 32 * sizeof(double);
 
+// Supernodes with width * rows >= this (or more rows than a warp's shared
+// accumulator) are solved by a whole CTA in the batched solve.
+long long big_task_wnr() {
+  long long v = 96;
+  if (const char* e = std::getenv("HYKKT_BIG_WNR")) v = std::max(1ll, std::atoll(e));
+  return v;
+}
+
 void coop_launch(Ctx& c, const void* fn, int blocks, void* args, std::size_t smem = 0) {
   void* argv[] = {args};
   CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), argv, smem, c.stream));
@@ -268,7 +281,7 @@ void init_ctx(Ctx& c, int device) {
   c.coop_trsv_blocks = occupancy_blocks(c, (const void*)dev::k_trsv);
   c.coop_cg_blocks = occupancy_blocks(c, (const void*)dev::k_cg);
   c.coop_ruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_ruiz), 2 * c.num_sms);
-  c.coop_bfactor_blocks = occupancy_blocks(c, (const void*)dev::kb_factor);
+  c.coop_bfactor_blocks = occupancy_blocks(c, (const void*)dev::kb_factor, kBatchSmem);
   c.coop_btrsv_blocks = occupancy_blocks(c, (const void*)dev::kb_trsv, kBatchSmem);
   // batched CG: grid * 256 must be a multiple of the system stride (a power
   // of two <= 2^16): use a power-of-two number of blocks.
@@ -334,6 +347,7 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   c.epoch = 0;
   c.have_plan = true;
+  c.bb.jobs_T = -1;
   c.have_factor = false;
 }
 
@@ -889,6 +903,90 @@ void batch_interleave_inputs(Ctx& c) {
 template <typename T>
 void balloc(hykkt::DBuf<T>& buf, idx n, int Bp) { buf.alloc(static_cast<std::size_t>(std::max<idx>(n, 1)) * Bp); }
 
+// Batch schedule (rebuilt when the tile count changes).  A supernode is
+// WIDE when its panel is large (width * rows >= HYKKT_BIG_WNR, or more rows
+// than a warp's shared accumulator) or any child is wide: the top of the
+// tree.  Wide supernodes get one CTA job per (supernode, system) and a
+// per-system panel layout; the narrow bulk stays lane-mode (lane = system),
+// 8 (supernode, tile) warp tasks to a CTA job.  Jobs are in topological
+// order: the factor list, then the solve list (forward tasks in level
+// order, backward tasks in reverse).
+void build_batch_jobs(Ctx& c, int T) {
+  const SupernodalPlan& sp = c.sp;
+  const long long ns = sp.nsup;
+  const int Bp = T * 32;
+  const long long wnr = big_task_wnr();
+  const int srows = batch_smem_rows();
+  std::vector<int> mode(ns, 0);
+  for (long long pos = 0; pos < ns; ++pos) {  // children before parents
+    const int sn = sp.order[pos];
+    const long long w = sp.sn_first[sn + 1] - sp.sn_first[sn], nr = sp.sn_nrows[sn];
+    if (w * nr >= wnr || nr > srows) mode[sn] = 1;
+    if (mode[sn] && sp.sn_parent[sn] >= 0) mode[sp.sn_parent[sn]] = 1;
+  }
+  // propagate upward again (a parent marked late still sits after its
+  // children in level order, so one more forward sweep closes the set)
+  for (long long pos = 0; pos < ns; ++pos) {
+    const int sn = sp.order[pos];
+    if (mode[sn] && sp.sn_parent[sn] >= 0) mode[sp.sn_parent[sn]] = 1;
+  }
+  std::vector<int> slot_sn(std::max<idx>(1, sp.panel_size), 0);
+  for (long long k = 0; k < ns; ++k) {
+    for (idx p = sp.sn_off[k]; p < sp.sn_off[k + 1]; ++p) slot_sn[p] = static_cast<int>(k);
+  }
+  auto build = [&](bool solve, std::vector<int>& ptr, std::vector<int>& items, std::vector<unsigned char>& kind) {
+    ptr.assign(1, 0);
+    items.clear();
+    kind.clear();
+    std::vector<int> group;
+    auto flush = [&] {
+      if (group.empty()) return;
+      items.insert(items.end(), group.begin(), group.end());
+      ptr.push_back(static_cast<int>(items.size()));
+      kind.push_back(0);
+      group.clear();
+    };
+    for (int pass = 0; pass < (solve ? 2 : 1); ++pass) {
+      for (long long pos = 0; pos < ns; ++pos) {
+        const int sn = pass == 0 ? sp.order[pos] : sp.order[ns - 1 - pos];
+        if (mode[sn]) {
+          flush();
+          for (int b = 0; b < Bp; ++b) {
+            items.push_back(sn * Bp + b);
+            ptr.push_back(static_cast<int>(items.size()));
+            kind.push_back(static_cast<unsigned char>(pass == 0 ? 1 : 2));
+          }
+        } else {
+          for (int tile = 0; tile < T; ++tile) {
+            group.push_back(static_cast<int>(pass * ns * T + pos * T + tile));
+            if (group.size() == 8) flush();
+          }
+        }
+      }
+      flush();
+    }
+  };
+  std::vector<int> ptr, items;
+  std::vector<unsigned char> kind;
+  auto& bb = c.bb;
+  build(true, ptr, items, kind);
+  bb.job_ptr.upload(ptr, c.stream);
+  bb.job_items.upload(items, c.stream);
+  bb.job_kind.upload(kind, c.stream);
+  bb.njobs = static_cast<int>(kind.size());
+  build(false, ptr, items, kind);
+  bb.fjob_ptr.upload(ptr, c.stream);
+  bb.fjob_items.upload(items, c.stream);
+  bb.fjob_kind.upload(kind, c.stream);
+  bb.nfjobs = static_cast<int>(kind.size());
+  bb.mode.upload(mode, c.stream);
+  bb.slot_sn.upload(slot_sn, c.stream);
+  bb.nwide = std::count(mode.begin(), mode.end(), 1);
+  bb.wdone.alloc(static_cast<std::size_t>(std::max<long long>(1, ns)) * Bp);
+  CK(cudaMemsetAsync(bb.wdone.p, 0, bb.wdone.n * sizeof(int), c.stream));
+  bb.jobs_T = T;
+}
+
 // The batched device path: every phase of solve_full for all systems at once
 // (lane = system).  Per-system outcomes follow the reference exactly: Ruiz
 // sweeps, the delta1 ladder (solver.cpp:108-142) with a fresh
@@ -928,6 +1026,7 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     CK(cudaMemsetAsync(bb.bdone.p, 0, bb.bdone.n * sizeof(int), st));
     bb.flags_init = true;
   }
+  if (bb.jobs_T != T) build_batch_jobs(c, T);
   dev::BVals v{bb.f[0], bb.f[1], bb.f[2], bb.f[3], bb.f[4], bb.f[5], bb.f[6], bb.f[7], bb.f[8]};
   int* abort = &c.status.p->abort;
   CK(cudaMemsetAsync(abort, 0, sizeof(int), st));
@@ -976,11 +1075,13 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     if (!any) break;
     CK(cudaMemcpyAsync(bb.delta1.p, d1.data(), Bp * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(bb.active.p, act.data(), Bp * sizeof(int), cudaMemcpyHostToDevice, st));
-    dev::kb_zero_panels<<<blocks_for(sp.panel_size * Bp), kThreads, 0, st>>>(sp.panel_size, bd, bb.active.p, bb.panel.p);
+    dev::kb_zero_panels<<<blocks_for(sp.panel_size * Bp), kThreads, 0, st>>>(sp.panel_size, bd, snp, bb.mode.p,
+                                                                             bb.slot_sn.p, bb.active.p, bb.panel.p);
     check_launch(c);
     if (nsrc > 0) {
-      dev::kb_scatter<<<grid_of(nsrc), kThreads, 0, st>>>(nsrc, bd, bb.hg.p, c.src_to_panel.p, c.src_row.p,
-                                                          c.src_col.p, bb.delta1.p, bb.active.p, bb.panel.p);
+      dev::kb_scatter<<<grid_of(nsrc), kThreads, 0, st>>>(nsrc, bd, snp, bb.mode.p, bb.slot_sn.p, bb.hg.p,
+                                                          c.src_to_panel.p, c.src_row.p, c.src_col.p, bb.delta1.p,
+                                                          bb.active.p, bb.panel.p);
       check_launch(c);
     }
     CK(cudaMemsetAsync(bb.fail.p, 0x7f, Bp * sizeof(int), st));
@@ -997,7 +1098,14 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     fa.fail_col = bb.fail.p;
     fa.abort = abort;
     fa.ticket = fresh_tickets(c, 1);
-    if (sp.nsup > 0) coop_launch(c, (const void*)dev::kb_factor, c.coop_bfactor_blocks, &fa);
+    fa.mode = bb.mode.p;
+    fa.wdone = bb.wdone.p;
+    fa.job_ptr = bb.fjob_ptr.p;
+    fa.job_items = bb.fjob_items.p;
+    fa.job_kind = bb.fjob_kind.p;
+    fa.njobs = bb.nfjobs;
+    fa.smem_doubles = static_cast<int>(kBatchSmem / sizeof(double));
+    if (sp.nsup > 0) coop_launch(c, (const void*)dev::kb_factor, c.coop_bfactor_blocks, &fa, kBatchSmem);
     CK(cudaMemcpyAsync(fail.data(), bb.fail.p, Bp * sizeof(int), cudaMemcpyDeviceToHost, st));
     read_status(c);
     for (int b = 0; b < Bp; ++b) {
@@ -1045,6 +1153,12 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     ta.j_ri = c.j_ri.p;
     ta.jval = bb.js.p;
     ta.lane_on = lane_on;
+    ta.job_ptr = bb.job_ptr.p;
+    ta.job_items = bb.job_items.p;
+    ta.job_kind = bb.job_kind.p;
+    ta.njobs = bb.njobs;
+    ta.mode = bb.mode.p;
+    ta.smem_doubles = static_cast<int>(kBatchSmem / sizeof(double));
     return ta;
   };
   if (sp.nsup > 0) {
@@ -1343,6 +1457,42 @@ int hykkt_host_analyze(int64_t n_x, int64_t m_c, int64_t m_d, const int64_t* h_c
   });
 }
 
+// Diagnostics (host only): per-supernode work of the analysed plan,
+// 6 doubles per supernode: width, rows, level, descendant updates,
+// left-looking update FMAs (sum over updates of m * cnt * wd, lower half),
+// dense panel FMAs (w^2 nr / 2).  Returns the supernode count in *nsup.
+int hykkt_debug_host_sn_stats(int64_t n_x, int64_t m_c, int64_t m_d, const int64_t* h_colptr,
+                              const int64_t* h_rowidx, const int64_t* j_colptr, const int64_t* j_rowidx,
+                              const int64_t* jd_colptr, const int64_t* jd_rowidx, const int64_t* perm,
+                              int64_t* nsup, double* out) {
+  return guarded([&] {
+    KktPlan kp = build_kkt_plan(n_x, m_c, m_d, pattern_from(n_x, n_x, h_colptr, h_rowidx),
+                                pattern_from(m_c, n_x, j_colptr, j_rowidx),
+                                pattern_from(m_d, n_x, jd_colptr, jd_rowidx));
+    std::vector<idx> pv;
+    if (perm) pv.assign(perm, perm + n_x);
+    const SupernodalPlan sp = build_supernodal_plan(kp.hg, std::move(pv));
+    *nsup = sp.nsup;
+    for (idx k = 0; k < sp.nsup; ++k) {
+      const double w = sp.sn_first[k + 1] - sp.sn_first[k], nr = sp.sn_nrows[k];
+      double uf = 0.0;
+      for (int u = sp.upd_ptr[k]; u < sp.upd_ptr[k + 1]; ++u) {
+        const int d = sp.upd_d[u];
+        const double m = sp.sn_nrows[d] - sp.upd_off[u], cnt = sp.upd_cnt[u];
+        const double wd = sp.sn_first[d + 1] - sp.sn_first[d];
+        uf += (m * cnt - cnt * (cnt - 1) / 2.0) * wd;
+      }
+      double* o = out + 6 * k;
+      o[0] = w;
+      o[1] = nr;
+      o[2] = sp.sn_level[k];
+      o[3] = sp.upd_ptr[k + 1] - sp.upd_ptr[k];
+      o[4] = uf;
+      o[5] = w * w * nr / 2.0;
+    }
+  });
+}
+
 int hykkt_get_perm(hykkt_t h, int64_t* perm) {
   return guarded([&] {
     Ctx& c = ctx(h);
@@ -1472,15 +1622,19 @@ int hykkt_chol_get_factor(hykkt_t h, int64_t* l_colptr, int64_t* l_rowidx, doubl
 }
 
 // Diagnostics: one traced batched H^-1 pass over the last batch (needs a
-// solved batch); out[t] / out[2 ntask + t] = end / start ns of task t.
-int hykkt_debug_btrsv_trace(hykkt_t h, uint64_t* out) {
+// solved batch); out[j] / out[njobs + j] = end / start ns of CTA job j.
+// With out == NULL, *njobs_out receives the job count only.
+int hykkt_debug_btrsv_trace(hykkt_t h, uint64_t* out, int64_t* njobs_out) {
   return guarded([&] {
     Ctx& c = ctx(h);
     auto& bb = c.bb;
+    if (bb.jobs_T < 0) throw StateError("no batch schedule");
+    if (njobs_out) *njobs_out = bb.njobs;
+    if (!out) return;
     const int T = bb.Bp / 32;
-    const idx nt = c.sp.nsup * T;
     hykkt::DBuf<unsigned long long> tr;
-    tr.alloc(4 * nt);
+    tr.alloc(2 * static_cast<std::size_t>(bb.njobs));
+    CK(cudaMemsetAsync(tr.p, 0, tr.n * sizeof(unsigned long long), c.stream));
     dev::BTrsvArgs ta;
     ta.s = c.snplan();
     ta.bd = dev::BDims{static_cast<int>(c.batch), bb.Bp, T};
@@ -1502,11 +1656,33 @@ int hykkt_debug_btrsv_trace(hykkt_t h, uint64_t* out) {
     ta.j_ri = c.j_ri.p;
     ta.jval = bb.js.p;
     ta.lane_on = nullptr;
+    ta.job_ptr = bb.job_ptr.p;
+    ta.job_items = bb.job_items.p;
+    ta.job_kind = bb.job_kind.p;
+    ta.njobs = bb.njobs;
+    ta.mode = bb.mode.p;
+    ta.smem_doubles = static_cast<int>(kBatchSmem / sizeof(double));
     ta.trace = tr.p;
     ta.ticket = fresh_tickets(c, 1);
     coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
     read_status(c);
-    CK(cudaMemcpy(out, tr.p, 4 * nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, tr.p, tr.n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
+// Diagnostics: the batched solve schedule: job_ptr (njobs + 1), items,
+// kind (njobs) and the supernode mode (nsup).  Any pointer may be NULL.
+int hykkt_debug_batch_jobs(hykkt_t h, int32_t* job_ptr, int32_t* items, uint8_t* kind, int32_t* mode) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    auto& bb = c.bb;
+    if (bb.jobs_T < 0) throw StateError("no batch schedule");
+    if (job_ptr) CK(cudaMemcpy(job_ptr, bb.job_ptr.p, (bb.njobs + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+    int nitems = 0;
+    CK(cudaMemcpy(&nitems, bb.job_ptr.p + bb.njobs, sizeof(int), cudaMemcpyDeviceToHost));
+    if (items) CK(cudaMemcpy(items, bb.job_items.p, nitems * sizeof(int), cudaMemcpyDeviceToHost));
+    if (kind) CK(cudaMemcpy(kind, bb.job_kind.p, bb.njobs, cudaMemcpyDeviceToHost));
+    if (mode) CK(cudaMemcpy(mode, bb.mode.p, c.sp.nsup * sizeof(int), cudaMemcpyDeviceToHost));
   });
 }
 

@@ -27,6 +27,24 @@ struct BDims {
 
 __device__ __forceinline__ long long bidx(long long e, int Bp, int b) { return e * Bp + b; }
 
+// Dynamic shared memory of the batched persistent kernels (8 warps x
+// smem_rows x 32 doubles): per-warp accumulators of the lane-mode tasks, or
+// one staging area for a wide (per-system) task.
+extern __shared__ double bsmem[];
+
+// Panel layout of the batch.  Lane-mode supernodes (the narrow bulk of the
+// tree) interleave their panel [entry][system] (stride Bp, lane = system);
+// wide-mode supernodes (every supernode whose subtree holds a wide panel:
+// the top of the tree) store each system's panel contiguously inside the
+// same region, [system][entry], so one CTA can stage one system's panel with
+// coalesced loads.
+__device__ __forceinline__ long long pan_addr(const SnPlan& s, const int* mode, int sn, int local, int Bp,
+                                              int b) {
+  const long long off = s.off[sn];
+  if (mode[sn]) return off * Bp + (long long)b * (s.nrows[sn] * (s.first[sn + 1] - s.first[sn])) + local;
+  return (off + local) * Bp + b;
+}
+
 // [system][entry] (field-major, B systems) -> [entry][system] (Bp stride).
 __global__ void kb_interleave(const double* __restrict__ in, double* __restrict__ out, int n, int B,
                               int Bp) {
@@ -218,7 +236,8 @@ __global__ void kb_hgamma(AsmPlan p, BDims bd, double gamma, const double* __res
 }
 
 // H_delta slots of the systems still on the ladder -> their panels.
-__global__ void kb_scatter(int nsrc, BDims bd, const double* __restrict__ src, const int* __restrict__ to_panel,
+__global__ void kb_scatter(int nsrc, BDims bd, SnPlan sp, const int* __restrict__ mode, const int* __restrict__ slot_sn,
+                           const double* __restrict__ src, const int* __restrict__ to_panel,
                            const int* __restrict__ srow, const int* __restrict__ scol,
                            const double* __restrict__ delta1, const int* __restrict__ active,
                            double* __restrict__ panel) {
@@ -229,12 +248,19 @@ __global__ void kb_scatter(int nsrc, BDims bd, const double* __restrict__ src, c
   double v = src[g];
   const double d1 = delta1[b];
   if (d1 != 0.0 && srow[t] == scol[t]) v = __dadd_rn(v, d1);
-  panel[bidx(to_panel[t], Bp, b)] = v;
+  const int p = to_panel[t], sn = slot_sn[p];
+  panel[pan_addr(sp, mode, sn, p - sp.off[sn], Bp, b)] = v;
 }
 
-__global__ void kb_zero_panels(long long nslots, BDims bd, const int* __restrict__ active, double* __restrict__ panel) {
+__global__ void kb_zero_panels(long long nslots, BDims bd, SnPlan sp, const int* __restrict__ mode,
+                               const int* __restrict__ slot_sn, const int* __restrict__ active,
+                               double* __restrict__ panel) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (g < nslots * bd.Bp && active[g % bd.Bp]) panel[g] = 0.0;
+  if (g >= nslots * bd.Bp) return;
+  const int b = static_cast<int>(g % bd.Bp);
+  if (!active[b]) return;
+  const int p = static_cast<int>(g / bd.Bp), sn = slot_sn[p];
+  panel[pan_addr(sp, mode, sn, p - sp.off[sn], bd.Bp, b)] = 0.0;
 }
 
 // ---- factorization ----------------------------------------------------------
@@ -250,7 +276,14 @@ struct BFactorArgs {
   const int* active;    // Bp
   int* fail_col;        // Bp
   int* abort;
-  unsigned* ticket;
+  unsigned* ticket;     // job counter (zero on entry)
+  const int* mode;      // nsup: 1 = wide (per-system task), 0 = lane mode
+  int* wdone;           // nsup x Bp done flags of wide tasks
+  const int* job_ptr;   // CTA jobs in topological order (see btrsv_pass)
+  const int* job_items;
+  const unsigned char* job_kind;  // 0: up to 8 lane tasks; 1: one wide task (sn * Bp + b)
+  int njobs;
+  int smem_doubles;     // dynamic shared memory available to a wide task
 };
 
 // Per-lane dense work is written as blocks of independent loads followed by
@@ -355,16 +388,204 @@ __device__ void bfactor_task(const BFactorArgs& a, int sn, int tile, int lane) {
   warp_publish(a.done + sn * T + tile, a.epoch, lane);
 }
 
+// Wide factor task: one CTA, one system b.  The panel is staged in shared
+// memory; descendant blocks are staged in batches (all loads of a batch in
+// flight at once) and applied with warp-owned target columns (no races, a
+// fixed order per target entry); then a blocked right-looking Cholesky:
+// warp 0 factors kFB columns, all warps apply the rank-kFB trailing update.
+constexpr int kFB = 8;
+
+__device__ void wfactor_task(const BFactorArgs& a, int sn, int b, double* sm) {
+  const SnPlan& s = a.s;
+  const int Bp = a.bd.Bp, T = a.bd.T, tile = b >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const int size = nr * w;
+  const int* R = s.rows + s.rows_ptr[sn];
+  for (int c = s.child_ptr[sn] + tid; c < s.child_ptr[sn + 1]; c += blockDim.x) {
+    const int ch = s.child[c];
+    if (a.mode[ch]) wait_flag(a.wdone + (long long)ch * Bp + b, a.epoch, a.abort);
+    else wait_flag(a.done + ch * T + tile, a.epoch, a.abort);
+  }
+  __syncthreads();
+  fence_gpu();
+  const bool act = a.active[b] != 0;
+  double* Pg = a.panel + (long long)s.off[sn] * Bp + (long long)b * size;
+  if (act) {
+    // shared layout: panel | rows (int) | staging values | staging positions (int)
+    const bool fits = size + (nr + 1) / 2 + 1 + 512 <= a.smem_doubles;
+    double* PS = fits ? sm : Pg;
+    int* RS = reinterpret_cast<int*>(sm + (fits ? size : 0));
+    const int stage0 = (fits ? size : 0) + (nr + 1) / 2 + 1;
+    const int budget = a.smem_doubles - stage0;
+    double* DS = sm + stage0;
+    if (fits) {
+      for (int e = tid; e < size; e += blockDim.x) PS[e] = Pg[e];
+    }
+    for (int q = tid; q < nr; q += blockDim.x) RS[q] = R[q];
+    __syncthreads();
+    // ---- descendant updates, in batches that fit the staging area ----
+    const int u0 = s.upd_ptr[sn], u1 = s.upd_ptr[sn + 1];
+    int ub = u0;
+    while (ub < u1) {
+      // batch [ub, ue): staged values m * wd doubles + m positions each
+      int ue = ub, used = 0;
+      while (ue < u1) {
+        const int d = s.upd_d[ue];
+        const int m = s.nrows[d] - s.upd_off[ue], wd = s.first[d + 1] - s.first[d];
+        const int need = m * wd + (m + 1) / 2 + 1;
+        if (ue > ub && used + need > budget) break;
+        used += need;
+        ++ue;
+        if (used > budget) break;  // a single oversized block: staged area overflows -> handled below
+      }
+      const bool staged = used <= budget;
+      // stage
+      if (staged) {
+        int o2 = 0;
+        for (int u = ub; u < ue; ++u) {
+          const int d = s.upd_d[u], o = s.upd_off[u], cnt = s.upd_cnt[u];
+          const int nrd = s.nrows[d], wd = s.first[d + 1] - s.first[d], m = nrd - o;
+          const int* Rd = s.rows + s.rows_ptr[d];
+          double* V = DS + o2;
+          int* POS = reinterpret_cast<int*>(DS + o2 + m * wd);
+          for (int e = tid; e < m * wd; e += blockDim.x) {
+            const int k = e / m, ii = e - k * m;
+            V[e] = a.panel[pan_addr(s, a.mode, d, k * nrd + o + ii, Bp, b)];
+          }
+          for (int ii = tid; ii < m; ii += blockDim.x) {
+            const int r = __ldg(Rd + o + ii);
+            int pos;
+            if (ii < cnt) {
+              pos = r - f;
+            } else {
+              int lo = w, hi = nr;
+              while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (RS[mid] <= r) lo = mid; else hi = mid;
+              }
+              pos = lo;
+            }
+            POS[ii] = pos;
+          }
+          o2 += m * wd + (m + 1) / 2 + 1;
+        }
+      }
+      __syncthreads();
+      // apply: warp owns target columns cc = wid (mod 8)
+      int o2 = 0;
+      for (int u = ub; u < ue; ++u) {
+        const int d = s.upd_d[u], o = s.upd_off[u], cnt = s.upd_cnt[u];
+        const int nrd = s.nrows[d], wd = s.first[d + 1] - s.first[d], m = nrd - o;
+        const int* Rd = s.rows + s.rows_ptr[d];
+        const double* V = DS + o2;
+        const int* POS = reinterpret_cast<const int*>(DS + o2 + m * wd);
+        for (int jj = 0; jj < cnt; ++jj) {
+          const int cc = __ldg(Rd + o + jj) - f;
+          if ((cc & 7) != wid) continue;
+          for (int ii = jj + lane; ii < m; ii += 32) {
+            double dot = 0.0;
+            int pos;
+            if (staged) {
+              for (int k = 0; k < wd; ++k) dot = fma(V[k * m + ii], V[k * m + jj], dot);
+              pos = POS[ii];
+            } else {
+              for (int k = 0; k < wd; ++k) {
+                dot = fma(a.panel[pan_addr(s, a.mode, d, k * nrd + o + ii, Bp, b)],
+                          a.panel[pan_addr(s, a.mode, d, k * nrd + o + jj, Bp, b)], dot);
+              }
+              const int r = __ldg(Rd + o + ii);
+              if (ii < cnt) {
+                pos = r - f;
+              } else {
+                int lo = w, hi = nr;
+                while (hi - lo > 1) {
+                  const int mid = (lo + hi) >> 1;
+                  if (RS[mid] <= r) lo = mid; else hi = mid;
+                }
+                pos = lo;
+              }
+            }
+            PS[cc * nr + pos] -= dot;
+          }
+        }
+        if (staged) o2 += m * wd + (m + 1) / 2 + 1;
+      }
+      __syncthreads();
+      ub = ue;
+    }
+    // ---- dense blocked Cholesky of the panel ----
+    const double floor_v = fmax(a.maxdiag ? a.floor_rel * a.maxdiag[b] : a.floor_abs, 0.0);
+    for (int k0 = 0; k0 < w; k0 += kFB) {
+      const int kb = min(kFB, w - k0);
+      if (wid == 0) {
+        bool failed = false;
+        for (int k = k0; k < k0 + kb; ++k) {
+          double* Pk = PS + k * nr;
+          const double pivot = Pk[k];
+          if (!(pivot > floor_v) && !failed) {
+            failed = true;
+            if (lane == 0) atomicMin(a.fail_col + b, f + k);
+          }
+          const double dk = sqrt(pivot);
+          __syncwarp();
+          if (lane == 0) Pk[k] = dk;
+          for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] / dk;
+          __syncwarp();
+          for (int c = k + 1; c < k0 + kb; ++c) {
+            const double lck = Pk[c];
+            double* Pc = PS + c * nr;
+            for (int r = c + lane; r < nr; r += 32) Pc[r] = fma(-Pk[r], lck, Pc[r]);
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int c = k0 + kb + wid; c < w; c += 8) {
+        double lc[kFB];
+#pragma unroll
+        for (int k = 0; k < kFB; ++k) lc[k] = k < kb ? PS[(k0 + k) * nr + c] : 0.0;
+        double* Pc = PS + c * nr;
+        for (int r = c + lane; r < nr; r += 32) {
+          double v = Pc[r];
+#pragma unroll
+          for (int k = 0; k < kFB; ++k) {
+            if (k < kb) v = fma(-PS[(k0 + k) * nr + r], lc[k], v);
+          }
+          Pc[r] = v;
+        }
+      }
+      __syncthreads();
+    }
+    if (fits) {
+      for (int e = tid; e < size; e += blockDim.x) Pg[e] = PS[e];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    fence_gpu();
+    st_relaxed(a.wdone + (long long)sn * Bp + b, a.epoch);
+  }
+}
+
 __global__ void __launch_bounds__(256) kb_factor(BFactorArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int T = a.bd.T;
-  const long long ntask = (long long)a.s.nsup * T;
-  (void)gw;
-  (void)nw;
-  for (long long t = grab_task(a.ticket, lane); t < ntask; t = grab_task(a.ticket, lane)) {
-    bfactor_task(a, a.s.order[t / T], static_cast<int>(t % T), lane);
+  __shared__ int s_job;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int T = a.bd.T, Bp = a.bd.Bp;
+  for (;;) {
+    if (threadIdx.x == 0) s_job = static_cast<int>(atomicAdd(a.ticket, 1u));
+    __syncthreads();
+    const int j = s_job;
+    if (j >= a.njobs) break;
+    const int i0 = __ldg(a.job_ptr + j), i1 = __ldg(a.job_ptr + j + 1);
+    if (a.job_kind[j]) {
+      const int it = __ldg(a.job_items + i0);
+      wfactor_task(a, it / Bp, it % Bp, bsmem);
+    } else if (i0 + wid < i1) {
+      const int t = __ldg(a.job_items + i0 + wid);
+      bfactor_task(a, a.s.order[t / T], t % T, lane);
+    }
+    __syncthreads();
   }
 }
 
@@ -391,8 +612,18 @@ struct BTrsvArgs {
   const int* lane_on;  // Bp: 0 = system finished, skip its arithmetic (or null)
   GridBarrier bar;
   int smem_rows;       // per-warp shared accumulator rows (dynamic smem = 8 * rows * 256 B)
-  unsigned* ticket;    // task counter of this pass (zero on entry)
+  unsigned* ticket;    // job counter of this pass (zero on entry)
   unsigned long long* trace = nullptr;  // diagnostics
+  // CTA jobs in topological order: job j = items [job_ptr[j], job_ptr[j+1]).
+  // job_kind 0: up to 8 lane-mode tasks (task ids as in btrsv_pass), one per
+  // warp; 1 / 2: one wide forward / backward task (item = sn * Bp + b) done
+  // by the whole CTA for one system.
+  const int* job_ptr;
+  const int* job_items;
+  const unsigned char* job_kind;
+  int njobs;
+  const int* mode;     // nsup: 1 = wide
+  int smem_doubles;
 };
 
 __device__ __forceinline__ double brhs(const BTrsvArgs& a, int i, int b) {
@@ -581,7 +812,6 @@ __device__ void bbwd_task(const BTrsvArgs& a, int sn, int tile, int lane) {
   }
 }
 
-extern __shared__ double bsmem[];  // 8 warps x kSmemRows x 32 doubles
 
 __device__ __forceinline__ void brearm(const BTrsvArgs& a) {
   const double u = __longlong_as_double(kUnset);
@@ -595,25 +825,174 @@ __device__ __forceinline__ void brearm(const BTrsvArgs& a) {
   for (long long i = gt; i < nu; i += gs) a.u[i] = u;
 }
 
-// One forward + backward pass; y, x, u must hold kUnset on entry.
+// ---- wide (per-system) solve tasks ---------------------------------------
+// One CTA solves one system's supernode: the panel (contiguous per system in
+// wide mode) is staged in shared memory with coalesced loads issued before
+// the task waits on its inputs; warp 0 runs the dense triangular solve of
+// the diagonal block 32 columns at a time in registers (shuffles), all warps
+// apply each chunk to the remaining rows.  Vectors stay interleaved
+// [entry][system], shared with the lane-mode tasks.
+
+__device__ void wfwd_task(const BTrsvArgs& a, int sn, int b, double* sm) {
+  const SnPlan& s = a.s;
+  const int Bp = a.bd.Bp;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (a.lane_on && !a.lane_on[b]) return;  // CTA-uniform
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn], rp = s.rows_ptr[sn];
+  const int size = nr * w;
+  const double* Pg = a.panel + (long long)s.off[sn] * Bp + (long long)b * size;
+  const bool fits = size + nr + 32 <= a.smem_doubles;
+  double* PS = sm;
+  double* V = fits ? sm + size : sm;
+  double* Ys = V + nr;
+  const double* P = fits ? PS : Pg;
+  if (fits) {
+    for (int e = tid; e < size; e += blockDim.x) PS[e] = __ldg(Pg + e);
+  }
+  for (int q = tid; q < nr; q += blockDim.x) {
+    double v = q < w ? brhs(a, f + q, b) : 0.0;
+    const int g0 = __ldg(s.gat_ptr + rp + q), g1 = __ldg(s.gat_ptr + rp + q + 1);
+    for (int g = g0; g < g1; ++g) {
+      const double u = load_ready(a.u + (long long)__ldg(s.gat_idx + g) * Bp + b, a.abort);
+      v = q < w ? v - u : v + u;
+    }
+    V[q] = v;
+  }
+  __syncthreads();
+  for (int cb = 0; cb < w; cb += 32) {
+    const int cw = min(32, w - cb);
+    if (wid == 0) {
+      double d[32];  // row cb+lane of the chunk's diagonal block
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[k] = (k < cw && lane < cw) ? P[(cb + k) * nr + cb + lane] : 0.0;
+      double acc = lane < cw ? V[cb + lane] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k < cw) {
+          const double yk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, d[k], k);
+          if (lane == k) acc = yk;
+          if (lane > k && lane < cw) acc = fma(-d[k], yk, acc);
+        }
+      }
+      if (lane < cw) {
+        Ys[lane] = acc;
+        stcg(a.y + bidx(f + cb + lane, Bp, b), acc);
+      }
+    }
+    __syncthreads();
+    for (int q = cb + cw + tid; q < nr; q += blockDim.x) {
+      double v = V[q];
+      for (int k = 0; k < cw; ++k) {
+        const double l = P[(cb + k) * nr + q];
+        v = q < w ? fma(-l, Ys[k], v) : fma(l, Ys[k], v);
+      }
+      V[q] = v;
+    }
+    __syncthreads();
+  }
+  double* U = a.u + (long long)s.u_off[sn] * Bp + b;
+  for (int q = w + tid; q < nr; q += blockDim.x) stcg(U + (long long)(q - w) * Bp, V[q]);
+}
+
+__device__ void wbwd_task(const BTrsvArgs& a, int sn, int b, double* sm) {
+  const SnPlan& s = a.s;
+  const int Bp = a.bd.Bp;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (a.lane_on && !a.lane_on[b]) return;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const int size = nr * w, nbl = nr - w;
+  const int* R = s.rows + s.rows_ptr[sn];
+  const double* Pg = a.panel + (long long)s.off[sn] * Bp + (long long)b * size;
+  const bool fits = size + nr + 32 <= a.smem_doubles;
+  double* X = fits ? sm + size : sm;  // x of the rows below (nbl)
+  double* S = X + nbl;                // w partial sums
+  double* Xc = S + w;                 // chunk x (32)
+  const double* P = fits ? sm : Pg;
+  if (fits) {
+    for (int e = tid; e < size; e += blockDim.x) sm[e] = __ldg(Pg + e);
+  }
+  const int par = s.parent[sn];
+  if (par >= 0 && tid == 0) poll_value(a.x + bidx(s.first[par], Bp, b), a.abort);
+  __syncthreads();
+  for (int r = tid; r < nbl; r += blockDim.x) X[r] = load_ready(a.x + bidx(__ldg(R + w + r), Bp, b), a.abort);
+  __syncthreads();
+  for (int k = wid; k < w; k += 8) {
+    double t = 0.0;
+    for (int r = lane; r < nbl; r += 32) t = fma(P[k * nr + w + r], X[r], t);
+    t = warp_sum(t);
+    if (lane == 0) S[k] = t;
+  }
+  __syncthreads();
+  const int nchunks = (w + 31) >> 5;
+  for (int ci = nchunks - 1; ci >= 0; --ci) {
+    const int cb = ci * 32, cw = min(32, w - cb);
+    if (wid == 0) {
+      double d[32];  // column cb+lane: L(cb+j, cb+lane)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d[j] = (j < cw && lane < cw) ? P[(cb + lane) * nr + cb + j] : 0.0;
+      double acc = lane < cw ? load_ready(a.y + bidx(f + cb + lane, Bp, b), a.abort) - S[cb + lane] : 0.0;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (j < cw) {
+          const double xj = __shfl_sync(0xffffffffu, acc, j) / __shfl_sync(0xffffffffu, d[j], j);
+          if (lane == j) acc = xj;
+          if (lane < j) acc = fma(-d[j], xj, acc);
+        }
+      }
+      if (lane < cw) {
+        Xc[lane] = acc;
+        stcg(a.x + bidx(f + cb + lane, Bp, b), acc);
+        if (a.x_out) a.x_out[bidx(s.perm[f + cb + lane], Bp, b)] = acc;
+      }
+    }
+    __syncthreads();
+    if (ci > 0) {
+      for (int k = tid; k < cb; k += blockDim.x) {
+        double t = S[k];
+        for (int j = 0; j < cw; ++j) t = fma(P[k * nr + cb + j], Xc[j], t);
+        S[k] = t;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// One forward + backward pass over the CTA job list; y, x, u must hold
+// kUnset on entry.  Jobs are taken in topological order by whole CTAs
+// (deadlock-free for the same reason as warp tasks: every job's
+// dependencies lie in earlier jobs, all held by resident CTAs).
 __device__ __forceinline__ void btrsv_pass(const BTrsvArgs& a) {
-  const int lane = threadIdx.x & 31;
-  double* smem_warp = bsmem + (threadIdx.x >> 5) * a.smem_rows * 32;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
+  __shared__ int s_job;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* smem_warp = bsmem + wid * a.smem_rows * 32;
   const int T = a.bd.T;
   const long long ns = (long long)a.s.nsup * T;
-  (void)gw;
-  (void)nw;
-  for (long long t = grab_task(a.ticket, lane); t < 2 * ns; t = grab_task(a.ticket, lane)) {
-    if (a.trace && lane == 0) a.trace[2 * ns + t] = global_ns();
-    if (t < ns) bfwd_task(a, a.s.order[t / T], static_cast<int>(t % T), lane, smem_warp);
-    else {
-      const long long tb = 2 * ns - 1 - t;
-      bbwd_task(a, a.s.order[tb / T], static_cast<int>(tb % T), lane);
+  for (;;) {
+    if (threadIdx.x == 0) s_job = static_cast<int>(atomicAdd(a.ticket, 1u));
+    __syncthreads();
+    const int j = s_job;
+    if (j >= a.njobs) break;
+    const int i0 = __ldg(a.job_ptr + j), i1 = __ldg(a.job_ptr + j + 1);
+    const int kind = a.job_kind[j];
+    if (kind) {
+      const int it = __ldg(a.job_items + i0);
+      if (a.trace && threadIdx.x == 0) a.trace[a.njobs + j] = global_ns();
+      if (kind == 1) wfwd_task(a, it / a.bd.Bp, it % a.bd.Bp, bsmem);
+      else wbwd_task(a, it / a.bd.Bp, it % a.bd.Bp, bsmem);
+      if (a.trace && threadIdx.x == 0) a.trace[j] = global_ns();
+    } else if (i0 + wid < i1) {
+      const long long t = __ldg(a.job_items + i0 + wid);
+      if (a.trace && threadIdx.x == 0) a.trace[a.njobs + j] = global_ns();
+      if (t < ns) {
+        bfwd_task(a, a.s.order[t / T], static_cast<int>(t % T), lane, smem_warp);
+      } else {
+        const long long tb = 2 * ns - 1 - t;
+        bbwd_task(a, a.s.order[tb / T], static_cast<int>(tb % T), lane);
+      }
+      __syncwarp();
+      if (a.trace && lane == 0) atomicMax(a.trace + j, global_ns());
     }
-    __syncwarp();
-    if (a.trace && lane == 0) a.trace[t] = global_ns();
+    __syncthreads();
   }
 }
 

@@ -1,4 +1,4 @@
-"""Trace one batched H^-1 pass (diagnostics): where does the time go?"""
+"""Trace one batched H^-1 pass (diagnostics): per CTA job start/end times."""
 import ctypes as C, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -10,49 +10,51 @@ nb = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 systems = acopf.batch(nb, B, seed=7)
 dev = Device(0); dev.analyze(systems[0])
-bt = Batch(dev); bt.upload(stack_values(systems)); bt.solve_resident(SolverConfig(), timing=True)
+bt = Batch(dev); bt.upload(stack_values(systems))
+for _ in range(2):
+    bt.solve_resident(SolverConfig(), timing=True)
 print("batch timing", {k: round(v, 2) for k, v in dev.timing().items()})
-info = dev.info(); ns = info["n_supernodes"]; T = max(1, (1 << (max(B, 32) - 1).bit_length()) // 32)
+info = dev.info(); ns = info["n_supernodes"]
+Bp = max(32, 1 << (B - 1).bit_length()); T = Bp // 32
 L = _lib.lib(); I32P = C.POINTER(C.c_int32)
-L.hykkt_debug_btrsv_trace.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+L.hykkt_debug_btrsv_trace.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]
+L.hykkt_debug_batch_jobs.argtypes = [C.c_void_p, I32P, I32P, C.POINTER(C.c_uint8), I32P]
 L.hykkt_debug_plan.argtypes = [C.c_void_p, I32P, I32P, I32P, I32P]
+nj = C.c_int64(0)
+_lib.check(L.hykkt_debug_btrsv_trace(dev.h, None, C.byref(nj)))
+nj = nj.value
+jp = np.zeros(nj + 1, np.int32); kind = np.zeros(nj, np.uint8); mode = np.zeros(ns, np.int32)
+_lib.check(L.hykkt_debug_batch_jobs(dev.h, jp.ctypes.data_as(I32P), None, kind.ctypes.data_as(C.POINTER(C.c_uint8)), mode.ctypes.data_as(I32P)))
+items = np.zeros(jp[-1], np.int32)
+_lib.check(L.hykkt_debug_batch_jobs(dev.h, None, items.ctypes.data_as(I32P), None, None))
 order = np.zeros(ns, np.int32); first = np.zeros(ns + 1, np.int32); nrows = np.zeros(ns, np.int32); parent = np.zeros(ns, np.int32)
 _lib.check(L.hykkt_debug_plan(dev.h, *[a.ctypes.data_as(I32P) for a in (order, first, nrows, parent)]))
-nt = ns * T
-out = np.zeros(4 * nt, np.uint64)
-for _ in range(2):
-    _lib.check(L.hykkt_debug_btrsv_trace(dev.h, out.ctypes.data_as(C.POINTER(C.c_uint64))))
-end, start = out[:2 * nt].astype(np.int64), out[2 * nt:].astype(np.int64)
+out = np.zeros(2 * nj, np.uint64)
+for _ in range(3):
+    _lib.check(L.hykkt_debug_btrsv_trace(dev.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), None))
+end, start = out[:nj].astype(np.int64), out[nj:].astype(np.int64)
 t0 = start.min(); end = (end - t0) / 1e3; start = (start - t0) / 1e3
 dur = end - start
-width = np.diff(first)
-print("pass us %.1f  fwd done %.1f" % (end.max(), end[:nt].max()))
-sn_of_task = np.concatenate([order[np.arange(nt) // T], order[(2 * nt - 1 - np.arange(nt, 2 * nt)) // T]])
-work = (width * nrows)[sn_of_task]
-for lo, hi in [(0, 64), (64, 256), (256, 1024), (1024, 4096), (4096, 1 << 30)]:
-    m = (work >= lo) & (work < hi)
+w = np.diff(first)
+print(f"jobs {nj}: lane {int((kind==0).sum())} wide-fwd {int((kind==1).sum())} wide-bwd {int((kind==2).sum())}; wide supernodes {int(mode.sum())} of {ns}")
+print("pass us %.1f" % end.max())
+for k, name in [(0, "lane"), (1, "wide fwd"), (2, "wide bwd")]:
+    m = kind == k
     if m.any():
-        print("w*nr in [%d,%d): tasks %d  dur us mean %.1f max %.1f  sum %.0f" % (lo, hi, m.sum(), dur[m].mean(), dur[m].max(), dur[m].sum()))
-q = np.linspace(0, nt - 1, 10).astype(int)
-print("fwd end at order quantiles:", [round(end[i], 1) for i in q])
-print("bwd end at order quantiles:", [round(end[nt + i], 1) for i in q])
-print("task start max %.1f" % start.max())
-# forward critical path for tile 0 (root first)
-fend = np.zeros(ns); fstart = np.zeros(ns)
-for t in range(nt):
-    if t % T == 0:
-        fend[order[t // T]] = end[t]; fstart[order[t // T]] = start[t]
-kids = [[] for _ in range(ns)]
-for k in range(ns):
-    if parent[k] >= 0: kids[parent[k]].append(k)
-node = int(np.argmax(fend)); path = []
-while True:
-    path.append(node)
-    if not kids[node]: break
-    node = max(kids[node], key=lambda c: fend[c])
-print("tile0 fwd critical path: sn w nr nchild start childend end own_us")
-tot = 0
-for k in path[:14]:
-    ce = max([fend[c] for c in kids[k]], default=fstart[k])
-    tot += fend[k] - ce
-    print("  %6d %4d %4d %3d %9.1f %9.1f %9.1f %8.1f" % (k, width[k], nrows[k], len(kids[k]), fstart[k], ce, fend[k], fend[k] - ce))
+        print(f"{name:9s}: start {start[m].min():8.1f}..{start[m].max():8.1f}  end max {end[m].max():8.1f}  dur mean {dur[m].mean():6.1f} max {dur[m].max():7.1f}")
+nlane_f = None
+# lane forward jobs = kind 0 jobs whose first item < ns*T
+lf = (kind == 0) & (items[jp[:-1]] < ns * T)
+print("lane fwd end %.1f  lane bwd start %.1f" % (end[lf].max(), start[(kind == 0) & ~lf].min() if ((kind == 0) & ~lf).any() else -1))
+# per wide supernode: mean fwd / bwd duration
+for k, name in [(1, "fwd"), (2, "bwd")]:
+    m = np.flatnonzero(kind == k)
+    sn = items[jp[m]] // Bp
+    rows = []
+    for s in np.unique(sn):
+        mm = m[sn == s]
+        rows.append((dur[mm].mean(), s, start[mm].min(), end[mm].max()))
+    rows.sort(reverse=True)
+    print(f"wide {name} supernodes by mean job us: sn w nr mean first_start last_end")
+    for d, s, a, e in rows[:10]:
+        print(f"  {s:6d} {w[s]:4d} {nrows[s]:4d} {d:7.1f} {a:8.1f} {e:8.1f}")
