@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CPP_SOURCES = ["analyze.cpp", "host_metrics.cpp"]
+CPP_SOURCES = ["analyze.cpp", "host_metrics.cpp", "sysplan.cpp"]
 CU_SOURCES = ["hykkt_cuda.cu"]
 HEADERS = list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + [INCLUDE / "hykkt.h"]
 

@@ -27,6 +27,8 @@
 #include "kernels_assemble.cuh"
 #include "kernels_solve.cuh"
 #include "kernels_batch.cuh"
+#include "kernels_sys.cuh"
+#include "sysplan.hpp"
 
 namespace hykkt {
 
@@ -160,6 +162,18 @@ struct hykkt_context {
     double* f[9] = {};
   } bb;
   std::vector<hykkt_report_t> batch_reports;
+  // system-per-CTA solve (kernels_sys.cuh): stream program + per-system data
+  struct SysBufsT {
+    int state = 0;  // 0 unbuilt, 1 ready, -1 infeasible (lane path)
+    std::string why;
+    hykkt::SysPlan plan;
+    std::size_t smem = 0;
+    hykkt::DBuf<int> idx, src, ok, flags;
+    hykkt::DBuf<double> vals, rhat, rys, d, scratch, relres, d2;
+    hykkt::DBuf<long long> iters;
+    hykkt::DBuf<unsigned long long> prof, trace;
+    int prof_on = -1, prof_ctas = 0;
+  } ks;
 
   hykkt::dev::SnPlan snplan() const {
     hykkt::dev::SnPlan s;
@@ -348,6 +362,7 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   c.epoch = 0;
   c.have_plan = true;
   c.bb.jobs_T = -1;
+  c.ks.state = 0;
   c.have_factor = false;
 }
 
@@ -987,6 +1002,61 @@ void build_batch_jobs(Ctx& c, int T) {
   bb.jobs_T = T;
 }
 
+// ---- system-per-CTA solve (kernels_sys.cuh) ---------------------------------
+constexpr int kKsThreads = 512;
+constexpr int kKsChunkLg = 10;  // 1024-entry TMA chunks (8 KB values, 4 KB indices)
+constexpr int kKsPmax = 1024;
+
+std::size_t ks_smem_bytes(idx n, int nv, int ni) {
+  const std::size_t vbytes = (static_cast<std::size_t>(n) * 8 + 127) & ~static_cast<std::size_t>(127);
+  return (static_cast<std::size_t>(nv) * 8 + static_cast<std::size_t>(ni) * 4) * (std::size_t{1} << kKsChunkLg) +
+         8 * static_cast<std::size_t>(nv + ni) + 8 * 66 + 64 + 8 * dev::kPrN + 8 * kKsPmax + vbytes;
+}
+
+// Builds (once per pattern) the stream program of the system-per-CTA solve
+// with the largest rings that fit one CTA's shared memory next to the
+// solve vector.  Infeasible (the lane-per-system kernels are used) when not
+// even 4-chunk rings fit or a supernode block does not fit the rings;
+// HYKKT_BATCH_PATH=lane forces the lane path.
+bool ks_prepare(Ctx& c) {
+  auto& ks = c.ks;
+  if (ks.state != 0) return ks.state == 1;
+  ks.state = -1;
+  if (const char* e = std::getenv("HYKKT_BATCH_PATH")) {
+    if (std::string(e) == "lane") {
+      ks.why = "HYKKT_BATCH_PATH=lane";
+      return false;
+    }
+  }
+  const SupernodalPlan& sp = c.sp;
+  if (sp.nsup == 0) {
+    ks.why = "empty factor";
+    return false;
+  }
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+  int nch = 16;
+  while (nch >= 4 && ks_smem_bytes(sp.n, nch, nch) > static_cast<std::size_t>(optin)) nch /= 2;
+  if (nch < 4) {
+    ks.why = "solve vector does not fit shared memory";
+    return false;
+  }
+  try {
+    ks.plan = build_sys_plan(sp, c.kp, kKsChunkLg, nch, kKsChunkLg, nch, kKsPmax, kKsThreads - 32);
+  } catch (const InvalidArgument& e) {
+    ks.why = e.what();
+    return false;
+  }
+  cudaStream_t st = c.stream;
+  ks.idx.upload(ks.plan.idx, st);
+  ks.src.upload(ks.plan.src, st);
+  ks.smem = ks_smem_bytes(sp.n, nch, nch);
+  CK(cudaFuncSetAttribute((const void*)dev::ks_solve<kKsThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(ks.smem)));
+  ks.state = 1;
+  return true;
+}
+
 // The batched device path: every phase of solve_full for all systems at once
 // (lane = system).  Per-system outcomes follow the reference exactly: Ruiz
 // sweeps, the delta1 ladder (solver.cpp:108-142) with a fresh
@@ -1130,134 +1200,263 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
   }
   ev.rec(2, st);
 
-  // ---- w solve + Schur rhs ----
-  auto trsv_args = [&](const double* rb, const double* ru, double* x_out, const int* lane_on) {
-    dev::BTrsvArgs ta;
-    ta.s = snp;
-    ta.bd = bd;
-    ta.panel = bb.panel.p;
-    ta.y = bb.y.p;
-    ta.x = bb.xs.p;
-    ta.u = bb.u.p;
-    ta.acc = bb.acc.p;
-    ta.x_out = x_out;
-    ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
-    ta.smem_rows = batch_smem_rows();
-    ta.fdone = bb.fdone.p;
-    ta.bdone = bb.bdone.p;
-    ta.epoch = 0;
-    ta.abort = abort;
-    ta.rb = rb;
-    ta.ru = ru;
-    ta.j_cp = c.j_cp.p;
-    ta.j_ri = c.j_ri.p;
-    ta.jval = bb.js.p;
-    ta.lane_on = lane_on;
-    ta.job_ptr = bb.job_ptr.p;
-    ta.job_items = bb.job_items.p;
-    ta.job_kind = bb.job_kind.p;
-    ta.njobs = bb.njobs;
-    ta.mode = bb.mode.p;
-    ta.smem_doubles = static_cast<int>(kBatchSmem / sizeof(double));
-    return ta;
-  };
-  if (sp.nsup > 0) {
-    dev::BTrsvArgs ta = trsv_args(bb.rhat.p, nullptr, nullptr, nullptr);
-    ta.epoch = ++c.epoch;
-    ta.ticket = fresh_tickets(c, 1);
-    coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
-  }
-  if (mc > 0) {
-    dev::kb_schur_rhs<<<grid_of(mc), kThreads, 0, st>>>(static_cast<int>(mc), bd, c.jcsr_rp.p, c.jcsr_ci_perm.p,
-                                                        bb.jscsr.p, bb.xs.p, bb.rys.p, bb.cgrhs.p);
-    check_launch(c);
-  }
-  ev.rec(3, st);
-
-  // ---- CG (+ delta2 restart) ----
   std::vector<long long> iters(Bp, 0);
   std::vector<double> relres(Bp, 0.0), d2used(Bp, 0.0);
-  std::vector<int> cflags(Bp, 0), start(Bp, 0);
-  const long long cg0 = c.launches;
-  auto run_bcg = [&](const std::vector<int>& which, double delta2) {
-    CK(cudaMemcpyAsync(bb.start.p, which.data(), Bp * sizeof(int), cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(bb.live.p, 0, bb.live.n * sizeof(int), st));
-    dev::BCgArgs a;
-    a.tr = trsv_args(nullptr, bb.cgp.p, nullptr, bb.running.p);
+  std::vector<int> cflags(Bp, 0);
+  long long cg_launches = 0;
+  if (ks_prepare(c)) {
+    // ---- system-per-CTA: w solve, Schur rhs, CG (+ delta2), dx solve,
+    // unscale, recover — one launch, one CTA per system at a time ----
+    auto& ks = c.ks;
+    const SysPlan& P = ks.plan;
+    const long long vlen = static_cast<long long>(P.src.size());
+    ks.vals.alloc(static_cast<std::size_t>(B) * vlen);
+    {
+      dim3 rg(static_cast<unsigned>((vlen + 31) / 32), static_cast<unsigned>((B + 31) / 32));
+      dev::ks_remap<<<rg, 256, 0, st>>>(ks.src.p, vlen, snp, bb.mode.p, bb.slot_sn.p, Bp, B, bb.panel.p, bb.js.p,
+                                         ks.vals.p);
+      check_launch(c);
+    }
+    auto deint = [&](const double* in, hykkt::DBuf<double>& out, idx n) {
+      out.alloc(static_cast<std::size_t>(std::max<idx>(n, 1)) * B);
+      if (n <= 0) return;
+      dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>(Bp / 32));
+      dev::kb_deinterleave<<<grid, 256, 0, st>>>(in, out.p, static_cast<int>(n), B, Bp);
+      check_launch(c);
+    };
+    deint(bb.rhat.p, ks.rhat, nx);
+    deint(bb.rys.p, ks.rys, mc);
+    deint(bb.d.p, ks.d, nx + mc);
+    ks.ok.upload(ok.data(), B, st);
+    ks.iters.alloc(B);
+    ks.relres.alloc(B);
+    ks.flags.alloc(B);
+    ks.d2.alloc(B);
+    const int grid = static_cast<int>(std::min<long long>(B, c.num_sms));
+    ks.scratch.alloc(static_cast<std::size_t>(grid) * 5 * std::max<idx>(mc, 1));
+    ev.rec(3, st);
+    dev::KsArgs a{};
+    a.n = static_cast<int>(nx);
     a.mc = static_cast<int>(mc);
-    a.jcsr_rp = c.jcsr_rp.p;
-    a.jcsr_ci_perm = c.jcsr_ci_perm.p;
-    a.jcsr = bb.jscsr.p;
-    a.rhs = bb.cgrhs.p;
-    a.x = bb.cgx.p;
-    a.r = bb.cgr.p;
-    a.p = bb.cgp.p;
-    a.q = bb.cgq.p;
-    a.part = nullptr;
-    a.running = bb.running.p;
-    a.start = bb.start.p;
-    a.delta2 = delta2;
+    a.md = static_cast<int>(md);
+    a.idx = ks.idx.p;
+    a.vals = ks.vals.p;
+    a.vlen = vlen;
+    a.vchunk_lg = P.vchunk_lg;
+    a.nvchunk = P.nvchunk;
+    a.ichunk_lg = P.ichunk_lg;
+    a.nichunk = P.nichunk;
+    a.pmax = P.pmax;
+    for (int i = 0; i < 4; ++i) {
+      a.bv0[i] = P.blk[i].v0;
+      a.bv1[i] = P.blk[i].v1;
+      a.bi0[i] = P.blk[i].i0;
+      a.bi1[i] = P.blk[i].i1;
+      a.bs0[i] = P.blk[i].s0;
+      a.bs1[i] = P.blk[i].s1;
+    }
+    a.perm = c.perm.p;
+    a.iperm = c.iperm.p;
+    a.rhat = ks.rhat.p;
+    a.rys = ks.rys.p;
+    a.d = ks.d.p;
+    a.jd_rp = c.jdcsr_rp.p;
+    a.jd_ci = c.jdcsr_ci.p;
+    a.jd_src = c.jdcsr_src.p;
+    {
+      // original per-system values as uploaded: [field][system][entry]
+      const BatchLayout L = batch_layout(k);
+      const double* f[9];
+      idx off = 0;
+      for (int i = 0; i < 9; ++i) {
+        f[i] = c.bvals.p + off;
+        off += L.sizes[i] * B;
+      }
+      a.jd = f[2];
+      a.ds_in = f[4];
+      a.rs = f[6];
+      a.ryd = f[8];
+    }
+    a.nnz_jd = k.jd.nnz();
+    a.odx = c.bouts.p;
+    a.ody = c.bouts.p + static_cast<idx>(B) * nx;
+    a.ods = a.ody + static_cast<idx>(B) * mc;
+    a.odyd = a.ods + static_cast<idx>(B) * md;
+    a.scratch = ks.scratch.p;
     a.tol = cfg.cg_tol;
     a.thr = cfg.small_quadratic_threshold;
+    a.delta2 = cfg.delta2;
     a.max_iter = cfg.cg_max_iter;
-    a.epoch_base = c.epoch;
-    a.iters = bb.iters.p;
-    a.relres = bb.relres.p;
-    a.flags = bb.flags.p;
-    a.live = bb.live.p;
-    a.tickets = fresh_tickets(c, cfg.cg_max_iter + 2);
-    a.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
-    const int blocks = c.coop_bcg_blocks;
-    bb.part.alloc(static_cast<std::size_t>(blocks) * kThreads);
-    a.part = bb.part.p;
-    coop_launch(c, (const void*)dev::kb_cg, blocks, &a, kBatchSmem);
-    c.epoch += static_cast<int>(std::min<long long>(cfg.cg_max_iter, 1 << 28)) + 1;
-    CK(cudaMemcpyAsync(iters.data(), bb.iters.p, Bp * sizeof(long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(relres.data(), bb.relres.p, Bp * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(cflags.data(), bb.flags.p, Bp * sizeof(int), cudaMemcpyDeviceToHost, st));
-    read_status(c);
-  };
-  if (mc > 0) {
-    run_bcg(ok, 0.0);
-    std::vector<int> redo(Bp, 0);
-    bool any = false;
-    for (int b = 0; b < Bp; ++b) {
-      if (ok[b] && cflags[b] == 2) {
-        redo[b] = 1;
-        d2used[b] = cfg.delta2;
-        any = true;
-      }
+    a.ok = ks.ok.p;
+    a.iters = ks.iters.p;
+    a.relres = ks.relres.p;
+    a.flags = ks.flags.p;
+    a.d2used = ks.d2.p;
+    a.ticket = fresh_tickets(c, 1);
+    a.B = B;
+    if (ks.prof_on < 0) ks.prof_on = std::getenv("HYKKT_KS_PROF") ? 1 : 0;
+    a.debug = std::getenv("HYKKT_KS_DEBUG") ? std::atoi(std::getenv("HYKKT_KS_DEBUG")) : 0;
+    a.prof = nullptr;
+    if (ks.prof_on) {
+      ks.prof.alloc(static_cast<std::size_t>(grid) * dev::kPrN);
+      ks.prof_ctas = grid;
+      a.prof = ks.prof.p;
+      ks.trace.alloc(P.nsteps + 1);
+      a.trace = ks.trace.p;
     }
-    if (any) run_bcg(redo, cfg.delta2);
+    const long long cg0 = c.launches;
+    dev::ks_solve<kKsThreads><<<grid, kKsThreads, ks.smem, st>>>(a);
+    check_launch(c);
+    cg_launches = c.launches - cg0;
+    ev.rec(4, st);
+    // failed factorizations: no solution (NaN), as the reference returns none
+    for (int b = 0; b < B; ++b) {
+      if (ok[b]) continue;
+      CK(cudaMemsetAsync(a.odx + static_cast<idx>(b) * nx, 0xff, nx * sizeof(double), st));
+      CK(cudaMemsetAsync(a.ody + static_cast<idx>(b) * mc, 0xff, mc * sizeof(double), st));
+      CK(cudaMemsetAsync(a.ods + static_cast<idx>(b) * md, 0xff, md * sizeof(double), st));
+      CK(cudaMemsetAsync(a.odyd + static_cast<idx>(b) * md, 0xff, md * sizeof(double), st));
+    }
+    std::vector<int> fl(B);
+    std::vector<double> d2(B);
+    CK(cudaMemcpyAsync(iters.data(), ks.iters.p, B * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(relres.data(), ks.relres.p, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fl.data(), ks.flags.p, B * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(d2.data(), ks.d2.p, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b) {
+      cflags[b] = fl[b];
+      d2used[b] = d2[b];
+    }
   } else {
-    CK(cudaMemsetAsync(bb.cgx.p, 0, bb.cgx.n * sizeof(double), st));
-    for (int b = 0; b < Bp; ++b) cflags[b] = 1;
-  }
-  const long long cg_launches = c.launches - cg0;
-  ev.rec(4, st);
 
-  // ---- dx solve, unscale, recover ----
-  if (sp.nsup > 0) {
-    dev::BTrsvArgs ta = trsv_args(bb.rhat.p, bb.cgx.p, bb.dxs.p, nullptr);
-    ta.epoch = ++c.epoch;
-    ta.ticket = fresh_tickets(c, 1);
-    coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
-  }
-  dev::kb_recover<<<grid_of(std::max<idx>({nx, mc, md})), kThreads, 0, st>>>(
-      ap, bd, c.jdcsr_rp.p, c.jdcsr_ci.p, c.jdcsr_src.p, bb.d.p, bb.dxs.p, bb.cgx.p, v, bb.odx.p, bb.ody.p,
-      bb.ods.p, bb.odyd.p);
-  check_launch(c);
-  {
-    const idx ns[4] = {nx, mc, md, md};
-    const double* src[4] = {bb.odx.p, bb.ody.p, bb.ods.p, bb.odyd.p};
-    idx off = 0;
-    for (int i = 0; i < 4; ++i) {
-      if (ns[i] > 0) {
-        dim3 grid(static_cast<unsigned>((ns[i] + 31) / 32), static_cast<unsigned>(Bp / 32));
-        dev::kb_deinterleave<<<grid, 256, 0, st>>>(src[i], c.bouts.p + off, static_cast<int>(ns[i]), B, Bp);
-        check_launch(c);
+    // ---- w solve + Schur rhs ----
+    auto trsv_args = [&](const double* rb, const double* ru, double* x_out, const int* lane_on) {
+      dev::BTrsvArgs ta;
+      ta.s = snp;
+      ta.bd = bd;
+      ta.panel = bb.panel.p;
+      ta.y = bb.y.p;
+      ta.x = bb.xs.p;
+      ta.u = bb.u.p;
+      ta.acc = bb.acc.p;
+      ta.x_out = x_out;
+      ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+      ta.smem_rows = batch_smem_rows();
+      ta.fdone = bb.fdone.p;
+      ta.bdone = bb.bdone.p;
+      ta.epoch = 0;
+      ta.abort = abort;
+      ta.rb = rb;
+      ta.ru = ru;
+      ta.j_cp = c.j_cp.p;
+      ta.j_ri = c.j_ri.p;
+      ta.jval = bb.js.p;
+      ta.lane_on = lane_on;
+      ta.job_ptr = bb.job_ptr.p;
+      ta.job_items = bb.job_items.p;
+      ta.job_kind = bb.job_kind.p;
+      ta.njobs = bb.njobs;
+      ta.mode = bb.mode.p;
+      ta.smem_doubles = static_cast<int>(kBatchSmem / sizeof(double));
+      return ta;
+    };
+    if (sp.nsup > 0) {
+      dev::BTrsvArgs ta = trsv_args(bb.rhat.p, nullptr, nullptr, nullptr);
+      ta.epoch = ++c.epoch;
+      ta.ticket = fresh_tickets(c, 1);
+      coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
+    }
+    if (mc > 0) {
+      dev::kb_schur_rhs<<<grid_of(mc), kThreads, 0, st>>>(static_cast<int>(mc), bd, c.jcsr_rp.p, c.jcsr_ci_perm.p,
+                                                          bb.jscsr.p, bb.xs.p, bb.rys.p, bb.cgrhs.p);
+      check_launch(c);
+    }
+    ev.rec(3, st);
+
+    // ---- CG (+ delta2 restart) ----
+    std::vector<int> start(Bp, 0);
+    const long long cg0 = c.launches;
+    auto run_bcg = [&](const std::vector<int>& which, double delta2) {
+      CK(cudaMemcpyAsync(bb.start.p, which.data(), Bp * sizeof(int), cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(bb.live.p, 0, bb.live.n * sizeof(int), st));
+      dev::BCgArgs a;
+      a.tr = trsv_args(nullptr, bb.cgp.p, nullptr, bb.running.p);
+      a.mc = static_cast<int>(mc);
+      a.jcsr_rp = c.jcsr_rp.p;
+      a.jcsr_ci_perm = c.jcsr_ci_perm.p;
+      a.jcsr = bb.jscsr.p;
+      a.rhs = bb.cgrhs.p;
+      a.x = bb.cgx.p;
+      a.r = bb.cgr.p;
+      a.p = bb.cgp.p;
+      a.q = bb.cgq.p;
+      a.part = nullptr;
+      a.running = bb.running.p;
+      a.start = bb.start.p;
+      a.delta2 = delta2;
+      a.tol = cfg.cg_tol;
+      a.thr = cfg.small_quadratic_threshold;
+      a.max_iter = cfg.cg_max_iter;
+      a.epoch_base = c.epoch;
+      a.iters = bb.iters.p;
+      a.relres = bb.relres.p;
+      a.flags = bb.flags.p;
+      a.live = bb.live.p;
+      a.tickets = fresh_tickets(c, cfg.cg_max_iter + 2);
+      a.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
+      const int blocks = c.coop_bcg_blocks;
+      bb.part.alloc(static_cast<std::size_t>(blocks) * kThreads);
+      a.part = bb.part.p;
+      coop_launch(c, (const void*)dev::kb_cg, blocks, &a, kBatchSmem);
+      c.epoch += static_cast<int>(std::min<long long>(cfg.cg_max_iter, 1 << 28)) + 1;
+      CK(cudaMemcpyAsync(iters.data(), bb.iters.p, Bp * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(relres.data(), bb.relres.p, Bp * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(cflags.data(), bb.flags.p, Bp * sizeof(int), cudaMemcpyDeviceToHost, st));
+      read_status(c);
+    };
+    if (mc > 0) {
+      run_bcg(ok, 0.0);
+      std::vector<int> redo(Bp, 0);
+      bool any = false;
+      for (int b = 0; b < Bp; ++b) {
+        if (ok[b] && cflags[b] == 2) {
+          redo[b] = 1;
+          d2used[b] = cfg.delta2;
+          any = true;
+        }
       }
-      off += ns[i] * B;
+      if (any) run_bcg(redo, cfg.delta2);
+    } else {
+      CK(cudaMemsetAsync(bb.cgx.p, 0, bb.cgx.n * sizeof(double), st));
+      for (int b = 0; b < Bp; ++b) cflags[b] = 1;
+    }
+    cg_launches = c.launches - cg0;
+    ev.rec(4, st);
+
+    // ---- dx solve, unscale, recover ----
+    if (sp.nsup > 0) {
+      dev::BTrsvArgs ta = trsv_args(bb.rhat.p, bb.cgx.p, bb.dxs.p, nullptr);
+      ta.epoch = ++c.epoch;
+      ta.ticket = fresh_tickets(c, 1);
+      coop_launch(c, (const void*)dev::kb_trsv, c.coop_btrsv_blocks, &ta, kBatchSmem);
+    }
+    dev::kb_recover<<<grid_of(std::max<idx>({nx, mc, md})), kThreads, 0, st>>>(
+        ap, bd, c.jdcsr_rp.p, c.jdcsr_ci.p, c.jdcsr_src.p, bb.d.p, bb.dxs.p, bb.cgx.p, v, bb.odx.p, bb.ody.p,
+        bb.ods.p, bb.odyd.p);
+    check_launch(c);
+    {
+      const idx ns[4] = {nx, mc, md, md};
+      const double* src[4] = {bb.odx.p, bb.ody.p, bb.ods.p, bb.odyd.p};
+      idx off = 0;
+      for (int i = 0; i < 4; ++i) {
+        if (ns[i] > 0) {
+          dim3 grid(static_cast<unsigned>((ns[i] + 31) / 32), static_cast<unsigned>(Bp / 32));
+          dev::kb_deinterleave<<<grid, 256, 0, st>>>(src[i], c.bouts.p + off, static_cast<int>(ns[i]), B, Bp);
+          check_launch(c);
+        }
+        off += ns[i] * B;
+      }
     }
   }
   ev.rec(5, st);
@@ -1458,9 +1657,10 @@ int hykkt_host_analyze(int64_t n_x, int64_t m_c, int64_t m_d, const int64_t* h_c
 }
 
 // Diagnostics (host only): per-supernode work of the analysed plan,
-// 6 doubles per supernode: width, rows, level, descendant updates,
+// 8 doubles per supernode: width, rows, level, descendant updates,
 // left-looking update FMAs (sum over updates of m * cnt * wd, lower half),
-// dense panel FMAs (w^2 nr / 2).  Returns the supernode count in *nsup.
+// dense panel FMAs (w^2 nr / 2), forward row-gather entries (sum over
+// updates of cnt * wd), supernode parent.  Returns the supernode count.
 int hykkt_debug_host_sn_stats(int64_t n_x, int64_t m_c, int64_t m_d, const int64_t* h_colptr,
                               const int64_t* h_rowidx, const int64_t* j_colptr, const int64_t* j_rowidx,
                               const int64_t* jd_colptr, const int64_t* jd_rowidx, const int64_t* perm,
@@ -1475,20 +1675,97 @@ int hykkt_debug_host_sn_stats(int64_t n_x, int64_t m_c, int64_t m_d, const int64
     *nsup = sp.nsup;
     for (idx k = 0; k < sp.nsup; ++k) {
       const double w = sp.sn_first[k + 1] - sp.sn_first[k], nr = sp.sn_nrows[k];
-      double uf = 0.0;
+      double uf = 0.0, ge = 0.0;
       for (int u = sp.upd_ptr[k]; u < sp.upd_ptr[k + 1]; ++u) {
         const int d = sp.upd_d[u];
         const double m = sp.sn_nrows[d] - sp.upd_off[u], cnt = sp.upd_cnt[u];
         const double wd = sp.sn_first[d + 1] - sp.sn_first[d];
         uf += (m * cnt - cnt * (cnt - 1) / 2.0) * wd;
+        ge += cnt * wd;
       }
-      double* o = out + 6 * k;
+      double* o = out + 8 * k;
+      o[6] = ge;
+      o[7] = sp.sn_parent[k];
       o[0] = w;
       o[1] = nr;
       o[2] = sp.sn_level[k];
       o[3] = sp.upd_ptr[k + 1] - sp.upd_ptr[k];
       o[4] = uf;
       o[5] = w * w * nr / 2.0;
+    }
+  });
+}
+
+// Diagnostics (host only): builds the system-per-CTA stream program for the
+// KKT pattern with rings of nchunk x 1024 entries and runs its host
+// emulation (sys_plan_selfcheck).  out[0] = max relative error vs a plain
+// J^T / supernodal solve / J reference, out[1] = value stream entries,
+// out[2] = index stream entries, out[3] = steps, out[4] = tasks,
+// out[5] = segments, out[6] = max segments per step, out[7] = non-padding
+// value entries.
+int hykkt_debug_sysplan_check(int64_t n_x, int64_t m_c, int64_t m_d, const int64_t* h_colptr,
+                              const int64_t* h_rowidx, const int64_t* j_colptr, const int64_t* j_rowidx,
+                              const int64_t* jd_colptr, const int64_t* jd_rowidx, const int64_t* perm,
+                              int nchunk, double* out) {
+  return guarded([&] {
+    KktPlan kp = build_kkt_plan(n_x, m_c, m_d, pattern_from(n_x, n_x, h_colptr, h_rowidx),
+                                pattern_from(m_c, n_x, j_colptr, j_rowidx),
+                                pattern_from(m_d, n_x, jd_colptr, jd_rowidx));
+    std::vector<idx> pv;
+    if (perm) pv.assign(perm, perm + n_x);
+    const SupernodalPlan sp = build_supernodal_plan(kp.hg, std::move(pv));
+    const SysPlan P = build_sys_plan(sp, kp, kKsChunkLg, nchunk, kKsChunkLg, nchunk, kKsPmax, kKsThreads - 32);
+    out[0] = sys_plan_selfcheck(sp, kp, P, 12345u);
+    out[1] = static_cast<double>(P.src.size());
+    out[2] = static_cast<double>(P.idx.size());
+    out[3] = P.nsteps;
+    out[4] = static_cast<double>(P.ntasks);
+    out[5] = static_cast<double>(P.nsegs);
+    out[6] = P.max_segs_per_step;
+    out[7] = static_cast<double>(P.value_entries);
+  });
+}
+
+// Diagnostics: per-CTA phase timers of the last system-per-CTA batched solve
+// (HYKKT_KS_PROF=1): 16 counters per CTA (kernels_sys.cuh KsProf), and
+// (trace, nsteps + 1 entries) CTA 0's end time of each substep of its first
+// solve, start time last.  Returns the CTA count in *nctas (0 = off).
+int hykkt_debug_ks_prof(hykkt_t h, uint64_t* out, int64_t* nctas, uint64_t* trace) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    *nctas = c.ks.prof_on == 1 ? c.ks.prof_ctas : 0;
+    if (*nctas && out) {
+      CK(cudaMemcpy(out, c.ks.prof.p, static_cast<std::size_t>(*nctas) * dev::kPrN * 8, cudaMemcpyDeviceToHost));
+    }
+    if (*nctas && trace) {
+      CK(cudaMemcpy(trace, c.ks.trace.p, c.ks.trace.n * 8, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+// Diagnostics: the system-per-CTA program's steps, 8 ints each (kind, index
+// length, value length, header words 3-6, widest task); returns the count.
+int hykkt_debug_ks_program(hykkt_t h, int32_t* steps, int64_t* nsteps) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!ks_prepare(c)) throw StateError("system-per-CTA path unavailable: " + c.ks.why);
+    const SysPlan& P = c.ks.plan;
+    *nsteps = P.nsteps;
+    if (!steps) return;
+    int k = 0;
+    for (int b = 0; b < 4; ++b) {
+      long long ib = P.blk[b].i0;
+      for (int s = P.blk[b].s0; s < P.blk[b].s1; ++s, ++k) {
+        const int* hd = P.idx.data() + ib;
+        int maxw = 0;
+        if (hd[0] <= HYKKT_STEP_BWD) {
+          const int dt = HYKKT_SP_HDR + HYKKT_SP_SEG_INTS * hd[3];
+          for (int t = 0; t < hd[4] + hd[5]; ++t) maxw = std::max(maxw, hd[dt + HYKKT_SP_TASK_INTS * t + 3] & 0xffff);
+        }
+        const int v8[8] = {hd[0], hd[1], hd[2], hd[3], hd[4], hd[5], hd[6], maxw};
+        std::copy(v8, v8 + 8, steps + 8 * k);
+        ib += hd[1];
+      }
     }
   });
 }

@@ -1,4 +1,6 @@
-"""Per-supernode work of the analysed plan (host only, no GPU)."""
+"""Per-level work of the analysed supernode tree (host only): how many
+supernodes, widths, forward row-gather entries and panel sizes per level --
+the input for choosing the per-system solve's task modes."""
 import ctypes as C, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -16,10 +18,11 @@ L.hykkt_debug_host_sn_stats.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 7 + [C.P
 _lib.check(L.hykkt_debug_host_sn_stats(s.n_x, s.m_c, s.m_d, *[ip(x) for x in a], None, C.byref(ns), out.ctypes.data))
 st = out[:8 * ns.value].reshape(-1, 8)
 w, nr, lev, nu, uf, df, ge, par = st.T
-print(f"nsup {ns.value} levels {int(lev.max())+1} total update FMAs {uf.sum():.3e} dense {df.sum():.3e}")
-top = np.argsort(-(uf + df))[:15]
-print("top supernodes by work: w nr level nupd upd_fma dense_fma")
-for k in top:
-    print(f"  {k:6d} {int(w[k]):4d} {int(nr[k]):4d} {int(lev[k]):3d} {int(nu[k]):5d} {uf[k]:10.0f} {df[k]:9.0f}")
-# critical path by work (sum along root path of max child)
-par = None
+tri = w * (w + 1) / 2
+pan = w * nr
+print(f"n {s.n_x} nsup {ns.value} nnzL {int(pan.sum() - (w*(w-1)/2).sum())} fwd-gather {int(ge.sum())} tri {int(tri.sum())}")
+print("lev  nsup  sum_w max_w  max_nr  gather  max_gather_per_sn  tri  panel  nsn(w>4)")
+for l in range(int(lev.max()) + 1):
+    m = lev == l
+    print(f"{l:3d} {m.sum():5d} {int(w[m].sum()):6d} {int(w[m].max()):4d} {int(nr[m].max()):5d} {int(ge[m].sum()):7d} "
+          f"{int(ge[m].max()):6d} {int(tri[m].sum()):6d} {int(pan[m].sum()):7d} {int((w[m]>4).sum()):4d}")
