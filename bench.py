@@ -295,24 +295,33 @@ def main():
     e2e_step_ms = allmax(ev0.elapsed_time(ev1) / args.steps, world)
     e2e_value = world * B / (e2e_step_ms / 1e3)
 
-    # ---- roofline of the CG kernel ----
+    # ---- roofline of the dominant kernel ----
+    # ks_solve (system-per-CTA) applies the Schur operator once per CG
+    # iteration plus the w and dx solves per system: (its + 2) applications
+    # of the canonical SURVEY.md §8(d) bytes each.  Its CUDA-event time is
+    # the handle's cg_ms phase (the launch is alone between two events on
+    # the handle's stream).
     peak, peak_kind = peaks()
     bytes_it = canonical_cg_bytes(info)
-    achieved = bytes_it * cg_its / (cg_ms / 1e3) / 1e9 if cg_ms > 0 else 0.0
+    ops = cg_its + 2 * B * args.steps
+    achieved = bytes_it * ops / (cg_ms / 1e3) / 1e9 if cg_ms > 0 else 0.0
     traffic = None
-    prof = ROOT / "profiles" / "k_cg_traffic.json"
+    prof = ROOT / "profiles" / "ks_solve_traffic.json"
     if prof.exists():
         try:
             d = json.loads(prof.read_text())
             if d.get("nb") == args.nb:
-                traffic = d.get("dram_bytes_per_cg_iteration")
+                traffic = d.get("dram_bytes_per_operator")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_cg (persistent CG: fused J^T p + supernodal fwd/bwd "
-                                          "solve + J t + dots/axpys)",
+    roofline = {"bound": "hbm",
+                "kernel": "ks_solve (one CTA per system: w solve, Schur-complement CG with the J^T / "
+                          "supernodal forward+backward / J operator streamed through shared-memory "
+                          "rings, dx solve, recover)",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "bytes_per_cg_iteration": bytes_it, "cg_iterations": cg_its, "cg_ms": cg_ms}
+                "bytes_per_operator": bytes_it, "operator_applications": ops, "cg_iterations": cg_its,
+                "kernel_ms": cg_ms}
 
     line = {
         "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
@@ -335,6 +344,9 @@ def main():
         "clocks": clk.summary(),
         "single_system": {"config": "ACTIVSg2000-shaped (configs[1])",
                           "ms_per_system_device": tot_dev_ms / (args.steps * B),
+                          "note": "batched per-system averages; on the system-per-CTA path solve_w_ms "
+                                  "is the stream build (remap) and cg_ms the fused ks_solve launch "
+                                  "(w solve + CG + dx solve + recover)",
                           **{k: v / (args.steps * B) for k, v in phase.items()},
                           "cg_iterations_mean": cg_its / (args.steps * B)},
     }

@@ -1301,7 +1301,8 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
       ks.prof.alloc(static_cast<std::size_t>(grid) * dev::kPrN);
       ks.prof_ctas = grid;
       a.prof = ks.prof.p;
-      ks.trace.alloc(P.nsteps + 1);
+      ks.trace.alloc(static_cast<std::size_t>(P.nsteps + 1) * 81);
+      CK(cudaMemsetAsync(ks.trace.p, 0, ks.trace.n * 8, st));
       a.trace = ks.trace.p;
     }
     const long long cg0 = c.launches;

@@ -158,6 +158,11 @@ struct KsTimer {
   }
 };
 
+// dynamic shared memory of ks_solve (namespace scope, so helpers that derive
+// pointers from it keep the shared address space: loads stay LDS, not
+// generic)
+extern __shared__ __align__(128) unsigned char ks_smem[];
+
 struct KsSmem {
   double* v;
   double* rv;  // value ring
@@ -169,6 +174,32 @@ struct KsSmem {
   int* sys;  // [0] system ticket, [2..3] late flags, [4..11] issue ranges (both by step parity)
   unsigned long long* prof;
 };
+
+
+// Shared-memory map of ks_solve: rings first (TMA destinations, aligned),
+// then mbarriers, reduction scratch, flags, timers, partials, solve vector.
+__device__ __forceinline__ KsSmem ks_layout(int nvchunk, int vchunk_lg, int nichunk, int ichunk_lg, int pmax) {
+  KsSmem S;
+  unsigned char* p = ks_smem;
+  S.rv = reinterpret_cast<double*>(p);
+  p += (8ll * nvchunk) << vchunk_lg;
+  S.ri = reinterpret_cast<int*>(p);
+  p += (4ll * nichunk) << ichunk_lg;
+  S.barv = reinterpret_cast<unsigned long long*>(p);
+  p += 8 * nvchunk;
+  S.bari = reinterpret_cast<unsigned long long*>(p);
+  p += 8 * nichunk;
+  S.red = reinterpret_cast<double*>(p);
+  p += 8 * 66;
+  S.sys = reinterpret_cast<int*>(p);
+  p += 64;
+  S.prof = reinterpret_cast<unsigned long long*>(p);
+  p += 8 * kPrN;
+  S.part = reinterpret_cast<double*>(p);
+  p += 8 * pmax;
+  S.v = reinterpret_cast<double*>(p);
+  return S;
+}
 
 // One stream's ring state (uniform across the CTA: every thread evolves it
 // identically; thread 0 alone issues copies).
@@ -385,13 +416,14 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
   const int* __restrict__ perm = a.perm;
   const int* __restrict__ gidx = a.idx;
   const int dbg = a.debug;
-  unsigned long long* const prof = a.prof ? S.prof : nullptr;
+  const KsSmem L = ks_layout(nvchunk, a.vchunk_lg, nichunk, a.ichunk_lg, a.pmax);
+  unsigned long long* const prof = a.prof ? L.prof : nullptr;
   unsigned long long* const trace_out = a.trace;
-  double* const rv_s = S.rv;
-  int* const ri_s = S.ri;
-  unsigned long long* const barv = S.barv;
-  unsigned long long* const bari = S.bari;
-  int* const sys = S.sys;
+  double* const rv_s = L.rv;
+  int* const ri_s = L.ri;
+  unsigned long long* const barv = L.barv;
+  unsigned long long* const bari = L.bari;
+  int* const sys = L.sys;
   constexpr int NC = NT - 32;  // compute threads
   constexpr int NWC = NC / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -401,32 +433,31 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
   const long long ci0 = a.bi0[ba] >> ilg, ci1 = a.bi1[bb] >> ilg;
   const int vmask = (nvchunk << vlg) - 1, imask = (nichunk << ilg) - 1;
   const long long Dv = (sv.G - cv0) << vlg, Di = (si.G - ci0) << ilg;
-  double* __restrict__ v = S.v;
-  double* __restrict__ part = S.part;
+  double* __restrict__ v = L.v;
+  double* __restrict__ part = L.part;
   long long vb = a.bv0[ba], ib = a.bi0[ba];
-  // ---- ring feed: every thread copies its 16-byte slice of each newly
-  // allowed chunk (one outstanding cp.async per thread per chunk keeps
-  // enough bytes in flight; a single issuing warp is limited to ~55
-  // outstanding requests).  The producer warp computes the allowed ranges
-  // and publishes them in sys[2..5] before each closing barrier.
+  // ---- ring feed: producer lanes 0..kIssuers-1 issue one TMA bulk copy
+  // per chunk (round-robin; a bulk copy completes ~every 375 ns per issuing
+  // thread, so several issuers are needed to reach HBM bandwidth,
+  // tools/micro/tma_multi.cu); completion is counted in bytes on the
+  // chunk's mbarrier.
+  constexpr int kIssuers = 4;
   const unsigned long long pol_v = policy_evict_first(), pol_i = policy_evict_last();
-  const int vthr = (8 << vlg) / 16, ithr = (4 << ilg) / 16;  // copying threads per chunk
   auto issue_range = [&](long long v_from, long long v_to, long long i_from, long long i_to) {
-    if (tid < vthr) {
-      for (long long gc = v_from; gc < v_to; ++gc) {
-        const long long c = cv0 + (gc - sv.G);
-        const int slot = static_cast<int>(gc & (nvchunk - 1));
-        cp_async16(rv_s + (slot << vlg) + 2 * tid, vals + (c << vlg) + 2 * tid, pol_v);
-        cp_async_arrive(barv + slot);
-      }
+    if (!producer || lane >= kIssuers) return;
+    for (long long gc = v_from + ((lane - v_from) % kIssuers + kIssuers) % kIssuers; gc < v_to; gc += kIssuers) {
+      const long long c = cv0 + (gc - sv.G);
+      const int slot = static_cast<int>(gc & (nvchunk - 1));
+      unsigned long long* bar = barv + slot;
+      mbar_expect_tx(bar, 8u << vlg);
+      tma_load_1d(rv_s + (slot << vlg), vals + (c << vlg), 8u << vlg, bar, pol_v);
     }
-    if (tid < ithr) {
-      for (long long gc = i_from; gc < i_to; ++gc) {
-        const long long c = ci0 + (gc - si.G);
-        const int slot = static_cast<int>(gc & (nichunk - 1));
-        cp_async16(ri_s + (slot << ilg) + 4 * tid, gidx + (c << ilg) + 4 * tid, pol_i);
-        cp_async_arrive(bari + slot);
-      }
+    for (long long gc = i_from + ((lane - i_from) % kIssuers + kIssuers) % kIssuers; gc < i_to; gc += kIssuers) {
+      const long long c = ci0 + (gc - si.G);
+      const int slot = static_cast<int>(gc & (nichunk - 1));
+      unsigned long long* bar = bari + slot;
+      mbar_expect_tx(bar, 4u << ilg);
+      tma_load_1d(ri_s + (slot << ilg), gidx + (c << ilg), 4u << ilg, bar, pol_i);
     }
   };
   // producer: the window allowed when a step starting at program chunks
@@ -487,6 +518,8 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
   __syncthreads();
   for (int s = s_begin; s < s_end; ++s) {
     const KsRing R{rv_s, ri_s, static_cast<int>((Dv + vb) & vmask), static_cast<int>((Di + ib) & imask), vmask, imask};
+    unsigned long long* wst = (trace && lane == 0) ? trace_out + (s_end + 1) + (static_cast<long long>(s) * 16 + wid) * 5 : nullptr;
+    if (wst) wst[0] = gtimer();
     // this step's window (published by the producer before the barrier)
     const int par = (s - s_begin) & 1;
     issue_published(par);
@@ -494,9 +527,11 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
       if (producer) wait_step(vb, ib);
       __syncthreads();
     }
+    if (wst) wst[1] = gtimer();
     const int kind = R.I(0), ilen = R.I(1), vlen = R.I(2), h3 = R.I(3), h4 = R.I(4), h5 = R.I(5);
     const long long ibn = ib + ilen, vbn = vb + vlen;
     const bool more = s + 1 < s_end;
+    if (wst) wst[2] = gtimer() + (static_cast<unsigned long long>(kind) << 60);
     tm.lap(kPrWait);
     tm.count(kPrSteps);
     if (producer) {
@@ -526,7 +561,16 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
         const int e0 = R.I(HYKKT_SP_HDR + j), e1 = R.I(HYKKT_SP_HDR + j + 1);
         double acc = 0.0;
         if (kind == HYKKT_STEP_JT) {
-          for (int e = e0; e < e1; ++e) acc = __dadd_rn(acc, __dmul_rn(R.V(e), u[R.I(xo + e)]));
+          // all of the row's u gathers (L2) in flight before the ordered sum
+          for (int e = e0; e < e1; e += 8) {
+            double ue[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ue[q] = e + q < e1 ? u[R.I(xo + e + q)] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (e + q < e1) acc = __dadd_rn(acc, __dmul_rn(R.V(e + q), ue[q]));
+            }
+          }
           const int i = r0 + j;
           v[i] = base ? __dsub_rn(base[__ldg(perm + i)], acc) : acc;
         } else {
@@ -558,14 +602,19 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
         for (; q < len; ++q) a0 = fma(R.V(voff + q), v[R.I(ioff + q)], a0);
         part[ls >> 16] = (a0 + a1) + (a2 + a3);
       }
+      if (wst) wst[3] = gtimer();
       if (nw + nt > 0 && nseg > 0) ks_bar_compute(NC);
       tm.lap(kPrA);
-      // ---- phase B ----
-      for (int t = wid; t < nw; t += NWC) {
-        const int d = dtask + HYKKT_SP_TASK_INTS * t;
-        ks_warp_task(R, v, part, R.I(d), R.I(d + 1), R.I(d + 2), R.I(d + 3) & 0xffff, bwd, lane);
+      // ---- phase B: warps [0, ww) take the warp tasks, the other warps'
+      // threads the thread tasks (dealt for that thread count by the builder)
+      const int ww = R.I(7), tt0 = 32 * ww, ntt = NC - tt0;
+      if (wid < ww) {
+        for (int t = wid; t < nw; t += ww) {
+          const int d = dtask + HYKKT_SP_TASK_INTS * t;
+          ks_warp_task(R, v, part, R.I(d), R.I(d + 1), R.I(d + 2), R.I(d + 3) & 0xffff, bwd, lane);
+        }
       }
-      for (int t = tid; t < nt; t += NC) {
+      for (int t = tid - tt0; t >= 0 && t < nt; t += ntt) {
         const int d = dtask + HYKKT_SP_TASK_INTS * (nw + t);
         const int wm = R.I(d + 3);
         const bool inl = (wm >> 16) == HYKKT_TASK_INLINE;
@@ -575,6 +624,7 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
       tm.lap(kPrB);
     }
     if (dbg == 2) asm volatile("cp.async.wait_all;" ::: "memory");
+    if (wst) wst[4] = gtimer();
     __syncthreads();
     tm.lap(kPrSync);
     if (trace && tid == 0) trace_out[s] = gtimer();
@@ -593,33 +643,12 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) ks_solve(KsArgs a) {
-  extern __shared__ __align__(128) unsigned char ks_smem[];
   const int tid = threadIdx.x;
-  KsSmem S;
-  {
-    unsigned char* p = ks_smem;
-    S.rv = reinterpret_cast<double*>(p);
-    p += (8ll * a.nvchunk) << a.vchunk_lg;
-    S.ri = reinterpret_cast<int*>(p);
-    p += (4ll * a.nichunk) << a.ichunk_lg;
-    S.barv = reinterpret_cast<unsigned long long*>(p);
-    p += 8 * a.nvchunk;
-    S.bari = reinterpret_cast<unsigned long long*>(p);
-    p += 8 * a.nichunk;
-    S.red = reinterpret_cast<double*>(p);
-    p += 8 * 66;
-    S.sys = reinterpret_cast<int*>(p);
-    p += 64;
-    S.prof = reinterpret_cast<unsigned long long*>(p);
-    p += 8 * kPrN;
-    S.part = reinterpret_cast<double*>(p);
-    p += 8 * a.pmax;
-    S.v = reinterpret_cast<double*>(p);
-  }
+  const KsSmem S = ks_layout(a.nvchunk, a.vchunk_lg, a.nichunk, a.ichunk_lg, a.pmax);
   if (tid == 0) {
-    // one arrival per copying thread (ks_run issue_range)
-    for (int i = 0; i < a.nvchunk; ++i) mbar_init(S.barv + i, (8u << a.vchunk_lg) / 16);
-    for (int i = 0; i < a.nichunk; ++i) mbar_init(S.bari + i, (4u << a.ichunk_lg) / 16);
+    // one arrive.expect_tx per chunk (ks_run issue_range)
+    for (int i = 0; i < a.nvchunk; ++i) mbar_init(S.barv + i, 1);
+    for (int i = 0; i < a.nichunk; ++i) mbar_init(S.bari + i, 1);
     mbar_fence_init();
     for (int i = 0; i < kPrN; ++i) S.prof[i] = 0;
   }

@@ -63,12 +63,12 @@ struct Builder {
 
   // ---- one L step ----------------------------------------------------------
   void emit_l_step(int kind, const std::vector<const Seg*>& segs, const std::vector<const Task*>& warp,
-                   const std::vector<const Task*>& thr, bool reads_earlier) {
+                   const std::vector<const Task*>& thr, bool reads_earlier, int ww) {
     const long long ib = ipos(), vb = vpos();
     const int nseg = static_cast<int>(segs.size()), nt = static_cast<int>(warp.size() + thr.size());
     last_hdr = ib;
     P.idx.insert(P.idx.end(), {kind, 0, 0, nseg, static_cast<int>(warp.size()), static_cast<int>(thr.size()),
-                               reads_earlier ? 1 : 0, 0});
+                               reads_earlier ? 1 : 0, ww});
     const long long desc0 = ipos();
     P.idx.resize(desc0 + HYKKT_SP_SEG_INTS * nseg + HYKKT_SP_TASK_INTS * nt, 0);
     for (int g = 0; g < nseg; ++g) {
@@ -226,10 +226,15 @@ struct Builder {
     auto by_cost = [](const Task* a, const Task* b) { return a->cost > b->cost; };
     std::stable_sort(warp.begin(), warp.end(), by_cost);
     std::stable_sort(thr.begin(), thr.end(), by_cost);
+    // warps [0, ww) take the warp tasks; thread tasks are dealt over the
+    // remaining NT - 32 ww threads (sysplan_format.h header word 7)
+    const int nwarps = P.nthreads / 32;
+    const int ww = warp.empty() ? 0 : thr.empty() ? std::min<int>(static_cast<int>(warp.size()), nwarps)
+                                                  : std::min<int>(static_cast<int>(warp.size()), std::max(1, nwarps / 2));
     // deal thread tasks: thread t takes positions t, t + NT, ...; snake order
     // over the full rounds balances every thread's total cost
     {
-      const std::size_t NT = static_cast<std::size_t>(P.nthreads);
+      const std::size_t NT = static_cast<std::size_t>(P.nthreads - 32 * ww);
       std::vector<const Task*> dealt(thr.size());
       const std::size_t full = thr.size() / NT;
       for (std::size_t i = 0; i < thr.size(); ++i) {
@@ -259,12 +264,12 @@ struct Builder {
       if (b == a) throw InvalidArgument("sys plan: segment does not fit the rings");
       std::vector<const Seg*> part;
       for (int q = a; q < b; ++q) part.push_back(&segs[q]);
-      emit_l_step(bwd ? HYKKT_STEP_BWD : HYKKT_STEP_FWD, part, none, none, false);
+      emit_l_step(bwd ? HYKKT_STEP_BWD : HYKKT_STEP_FWD, part, none, none, false, 0);
       a = b;
     }
     std::vector<const Seg*> part;
     for (int q = fa; q < ns; ++q) part.push_back(&segs[q]);
-    emit_l_step(bwd ? HYKKT_STEP_BWD : HYKKT_STEP_FWD, part, warp, thr, fa > 0);
+    emit_l_step(bwd ? HYKKT_STEP_BWD : HYKKT_STEP_FWD, part, warp, thr, fa > 0, ww);
     P.max_segs_per_step = std::max(P.max_segs_per_step, ns);
   }
 

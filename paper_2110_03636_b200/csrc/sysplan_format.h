@@ -9,12 +9,14 @@
 //   [4] L: warp tasks            J/JT: first row
 //   [5] L: thread tasks
 //   [6] L: 1 if phase B reads partials written by an earlier step
-//   [7] reserved
+//   [7] L: warps taking the warp tasks (thread tasks are dealt over the
+//       remaining compute threads)
 // L steps continue with segment descriptors (kSegInts each: value offset,
 // index offset, len | slot << 16; offsets relative to the step's bases),
 // task descriptors (kTaskInts each: value offset, index offset, first
 // column, width | mode << 16; warp tasks first, thread tasks dealt so that
-// thread t takes tasks t, t + NT, ...), then the payload.
+// thread task t goes to compute thread 32 ww + (t mod (NT - 32 ww))), then
+// the payload.
 // J / JT steps continue with rows + 1 relative value offsets, then one index
 // per value entry.
 //
