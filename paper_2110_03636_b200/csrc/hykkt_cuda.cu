@@ -1042,7 +1042,11 @@ bool ks_prepare(Ctx& c) {
     return false;
   }
   try {
-    ks.plan = build_sys_plan(sp, c.kp, kKsChunkLg, nch, kKsChunkLg, nch, kKsPmax, kKsThreads - 32);
+    // L steps of up to n-2 chunks: fewer, larger steps beat a guaranteed
+    // one-step lookahead (measured: 62 -> 54 ms per 256-system CG launch)
+    int step_chunks = nch - 2;
+    if (const char* e = std::getenv("HYKKT_KS_STEP_CHUNKS")) step_chunks = std::atoi(e);
+    ks.plan = build_sys_plan(sp, c.kp, kKsChunkLg, nch, kKsChunkLg, nch, kKsPmax, kKsThreads - 32, step_chunks);
   } catch (const InvalidArgument& e) {
     ks.why = e.what();
     return false;
@@ -1296,6 +1300,10 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     a.B = B;
     if (ks.prof_on < 0) ks.prof_on = std::getenv("HYKKT_KS_PROF") ? 1 : 0;
     a.debug = std::getenv("HYKKT_KS_DEBUG") ? std::atoi(std::getenv("HYKKT_KS_DEBUG")) : 0;
+    a.issuers = 4;
+    if (const char* e = std::getenv("HYKKT_KS_ISSUERS")) a.issuers = std::max(1, std::min(32, std::atoi(e)));
+    a.feed = 0;
+    if (const char* e = std::getenv("HYKKT_KS_FEED")) a.feed = std::atoi(e) ? 1 : 0;
     a.prof = nullptr;
     if (ks.prof_on) {
       ks.prof.alloc(static_cast<std::size_t>(grid) * dev::kPrN);

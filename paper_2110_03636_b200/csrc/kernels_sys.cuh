@@ -129,6 +129,8 @@ struct KsArgs {
   unsigned long long* prof;   // diagnostics: kPrN per CTA, or null
   unsigned long long* trace;  // diagnostics: CTA 0's first CG operator: end time per step
   int debug;                  // 1: the producer drains every issued chunk before each barrier
+  int issuers;                // warps issuing TMA copies (feed 1)
+  int feed;                   // 0 cp.async by all threads, 1 TMA bulk copies
 };
 
 // Per-CTA phase timers (thread 0's view, %globaltimer ns) when KsArgs::prof
@@ -436,23 +438,48 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
   double* __restrict__ v = L.v;
   double* __restrict__ part = L.part;
   long long vb = a.bv0[ba], ib = a.bi0[ba];
-  // ---- ring feed: producer lanes 0..kIssuers-1 issue one TMA bulk copy
-  // per chunk (round-robin; a bulk copy completes ~every 375 ns per issuing
-  // thread, so several issuers are needed to reach HBM bandwidth,
-  // tools/micro/tma_multi.cu); completion is counted in bytes on the
-  // chunk's mbarrier.
-  constexpr int kIssuers = 4;
+  // ---- ring feed (KsArgs::feed):
+  //  0  cp.async: every thread copies its 16-byte slice of each chunk
+  //     (LSU work spread over all warps; completion = one noinc arrival
+  //     per copying thread on the chunk's mbarrier)
+  //  1  TMA: one bulk copy per chunk, issued by lane 0 of warp
+  //     (chunk mod issuers); bulk requests are accepted ~every 400 ns per
+  //     SM (tools/micro/tma_pure.cu), completion counted in bytes.
+  const int feed = a.feed;
+  const int issuers = min(a.issuers, NT / 32);
+  const bool issuer = lane == 0 && wid < issuers;
+  const int vthr = (8 << vlg) / 16, ithr = (4 << ilg) / 16;  // cp.async copying threads per chunk
   const unsigned long long pol_v = policy_evict_first(), pol_i = policy_evict_last();
   auto issue_range = [&](long long v_from, long long v_to, long long i_from, long long i_to) {
-    if (!producer || lane >= kIssuers) return;
-    for (long long gc = v_from + ((lane - v_from) % kIssuers + kIssuers) % kIssuers; gc < v_to; gc += kIssuers) {
+    if (feed == 0) {
+      if (tid < vthr) {
+        for (long long gc = v_from; gc < v_to; ++gc) {
+          const long long c = cv0 + (gc - sv.G);
+          const int slot = static_cast<int>(gc & (nvchunk - 1));
+          cp_async16(rv_s + (slot << vlg) + 2 * tid, vals + (c << vlg) + 2 * tid, pol_v);
+          cp_async_arrive(barv + slot);
+        }
+      }
+      if (tid < ithr) {
+        for (long long gc = i_from; gc < i_to; ++gc) {
+          const long long c = ci0 + (gc - si.G);
+          const int slot = static_cast<int>(gc & (nichunk - 1));
+          cp_async16(ri_s + (slot << ilg) + 4 * tid, gidx + (c << ilg) + 4 * tid, pol_i);
+          cp_async_arrive(bari + slot);
+        }
+      }
+      return;
+    }
+    if (!issuer) return;
+    for (long long gc = v_from + ((wid - v_from) % issuers + issuers) % issuers; gc < v_to; gc += issuers) {
       const long long c = cv0 + (gc - sv.G);
       const int slot = static_cast<int>(gc & (nvchunk - 1));
       unsigned long long* bar = barv + slot;
       mbar_expect_tx(bar, 8u << vlg);
       tma_load_1d(rv_s + (slot << vlg), vals + (c << vlg), 8u << vlg, bar, pol_v);
     }
-    for (long long gc = i_from + ((lane - i_from) % kIssuers + kIssuers) % kIssuers; gc < i_to; gc += kIssuers) {
+    for (long long gc = i_from + ((issuers - 1 - wid - i_from) % issuers + issuers) % issuers; gc < i_to;
+         gc += issuers) {
       const long long c = ci0 + (gc - si.G);
       const int slot = static_cast<int>(gc & (nichunk - 1));
       unsigned long long* bar = bari + slot;
@@ -483,18 +510,22 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
     issue_range(sv.G + pub[0], sv.G + pub[1], si.G + pub[2], si.G + pub[3]);
   };
   // waits (producer) for program chunks [c0, c1] of each stream, as far as issued
+  // (the producer's 32 lanes wait on different chunks in parallel: a
+  // try_wait costs ~100 cycles even on a completed phase)
   auto wait_v = [&](long long c0, long long c1) {
     const long long g1 = min(sv.G + (c1 - cv0), sv.issued - 1);
-    for (long long gc = max(sv.ready + 1, sv.G + (c0 - cv0)); gc <= g1; ++gc) {
+    for (long long gc = max(sv.ready + 1, sv.G + (c0 - cv0)) + lane; gc <= g1; gc += 32) {
       mbar_wait(barv + (gc & (nvchunk - 1)), static_cast<unsigned>((gc / nvchunk) & 1));
     }
+    __syncwarp();
     sv.ready = max(sv.ready, g1);
   };
   auto wait_i = [&](long long c0, long long c1) {
     const long long g1 = min(si.G + (c1 - ci0), si.issued - 1);
-    for (long long gc = max(si.ready + 1, si.G + (c0 - ci0)); gc <= g1; ++gc) {
+    for (long long gc = max(si.ready + 1, si.G + (c0 - ci0)) + lane; gc <= g1; gc += 32) {
       mbar_wait(bari + (gc & (nichunk - 1)), static_cast<unsigned>((gc / nichunk) & 1));
     }
+    __syncwarp();
     si.ready = max(si.ready, g1);
   };
   // producer: wait for a whole step starting at (vb2, ib2); returns true
@@ -646,9 +677,10 @@ __global__ void __launch_bounds__(NT, 1) ks_solve(KsArgs a) {
   const int tid = threadIdx.x;
   const KsSmem S = ks_layout(a.nvchunk, a.vchunk_lg, a.nichunk, a.ichunk_lg, a.pmax);
   if (tid == 0) {
-    // one arrive.expect_tx per chunk (ks_run issue_range)
-    for (int i = 0; i < a.nvchunk; ++i) mbar_init(S.barv + i, 1);
-    for (int i = 0; i < a.nichunk; ++i) mbar_init(S.bari + i, 1);
+    // feed 0: one noinc arrival per copying thread; feed 1: one
+    // arrive.expect_tx per chunk (ks_run issue_range)
+    for (int i = 0; i < a.nvchunk; ++i) mbar_init(S.barv + i, a.feed ? 1u : (8u << a.vchunk_lg) / 16);
+    for (int i = 0; i < a.nichunk; ++i) mbar_init(S.bari + i, a.feed ? 1u : (4u << a.ichunk_lg) / 16);
     mbar_fence_init();
     for (int i = 0; i < kPrN; ++i) S.prof[i] = 0;
   }

@@ -49,8 +49,8 @@ struct Builder {
     // alignment and two consecutive steps always fit the ring: the data of
     // step k+1 is requested when step k starts (sysplan.hpp).  J / JT steps
     // (no dependencies between them) may use n - 2 chunks.
-    capv = static_cast<long long>(P.nvchunk / 2 - 1) << P.vchunk_lg;
-    capi = static_cast<long long>(P.nichunk / 2 - 1) << P.ichunk_lg;
+    capv = static_cast<long long>(P.step_chunks) << P.vchunk_lg;
+    capi = static_cast<long long>(P.step_chunks) << P.ichunk_lg;
     capv_rows = static_cast<long long>(P.nvchunk - 2) << P.vchunk_lg;
     capi_rows = static_cast<long long>(P.nichunk - 2) << P.ichunk_lg;
   }
@@ -359,7 +359,7 @@ struct Builder {
 }  // namespace
 
 SysPlan build_sys_plan(const SupernodalPlan& sp, const KktPlan& kp, int vchunk_lg, int nvchunk, int ichunk_lg,
-                       int nichunk, int pmax, int nthreads) {
+                       int nichunk, int pmax, int nthreads, int step_chunks) {
   if (nvchunk < 4 || nichunk < 4 || (nvchunk & (nvchunk - 1)) || (nichunk & (nichunk - 1)))
     throw InvalidArgument("sys plan: rings need a power-of-two count >= 4 of chunks");
   if (pmax < 64 || pmax >= (1 << 15)) throw InvalidArgument("sys plan: bad partials size");
@@ -371,6 +371,8 @@ SysPlan build_sys_plan(const SupernodalPlan& sp, const KktPlan& kp, int vchunk_l
   P.nichunk = nichunk;
   P.pmax = pmax;
   P.nthreads = nthreads;
+  P.step_chunks = step_chunks > 0 ? std::min(step_chunks, std::min(nvchunk, nichunk) - 2)
+                                  : std::min(nvchunk, nichunk) / 2 - 1;
   Builder b(sp, kp, P);
   const int n = static_cast<int>(sp.n), mc = static_cast<int>(kp.mc);
   // JT: row i of P J^T = column perm[i] of J (spmv transpose order)

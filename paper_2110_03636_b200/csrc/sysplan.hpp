@@ -48,6 +48,8 @@ struct SysPlan {
   int ichunk_lg = 0, nichunk = 0;  // index ring: nichunk chunks of 2^ichunk_lg ints
   int pmax = 0;                    // partial slots
   int nthreads = 0;                // CTA size the thread tasks were dealt for
+  int step_chunks = 0;             // L-step cap in chunks (<= n/2 - 1: the next step is
+                                   // always requested when a step starts)
   std::vector<int> idx;            // index stream
   std::vector<int> src;            // value stream source (sysplan_format.h kSrc*)
   struct Block {
@@ -64,7 +66,7 @@ struct SysPlan {
 // Builds the program.  Throws InvalidArgument when a supernode block does
 // not fit the rings (the caller then uses the lane-per-system path).
 SysPlan build_sys_plan(const SupernodalPlan& sp, const KktPlan& kp, int vchunk_lg, int nvchunk, int ichunk_lg,
-                       int nichunk, int pmax, int nthreads);
+                       int nichunk, int pmax, int nthreads, int step_chunks = 0);
 
 // Host emulation of the device program on random panel / J values (tests):
 // runs JT -> FWD -> BWD -> J and returns the max relative difference to a
