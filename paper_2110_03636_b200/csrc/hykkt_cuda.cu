@@ -172,6 +172,11 @@ struct hykkt_context {
     hykkt::DBuf<double> vals, rhat, rys, d, scratch, relres, d2;
     hykkt::DBuf<long long> iters;
     hykkt::DBuf<unsigned long long> prof, trace;
+    // ks_factor: per-level narrow (warp) and wide (CTA) supernode lists
+    hykkt::DBuf<int> lev_ptr, lev_sn, wlev_ptr, wlev_sn, upd, upd_rows, wb_ptr, wb_end, cb_ptr, cb_end;
+    hykkt::DBuf<double> hg, js;
+    std::size_t fsmem = 0;
+    int factor_on = 0;  // ks_factor opt-in (HYKKT_KS_FACTOR=1): correct, slower than kb_factor so far
     int prof_on = -1, prof_ctas = 0;
   } ks;
 
@@ -1054,6 +1059,82 @@ bool ks_prepare(Ctx& c) {
   cudaStream_t st = c.stream;
   ks.idx.upload(ks.plan.idx, st);
   ks.src.upload(ks.plan.src, st);
+  {
+    // ks_factor level lists: wide supernodes (CTA tasks) vs narrow (warp tasks)
+    std::vector<int> lp(sp.nlevels + 1, 0), wp(sp.nlevels + 1, 0), ls, ws;
+    long long wide_max = 0;
+    for (int L = 0; L < sp.nlevels; ++L) {
+      for (idx k = 0; k < sp.nsup; ++k) {
+        if (sp.sn_level[k] != L) continue;
+        const long long w = sp.sn_first[k + 1] - sp.sn_first[k], nr = sp.sn_nrows[k];
+        if (w * nr > dev::kKfWarpStage / 2) {
+          ws.push_back(static_cast<int>(k));
+          wide_max = std::max(wide_max, w * nr);
+        } else {
+          ls.push_back(static_cast<int>(k));
+        }
+      }
+      lp[L + 1] = static_cast<int>(ls.size());
+      wp[L + 1] = static_cast<int>(ws.size());
+    }
+    // per-update descriptors and staging batches (no dependent loads on the
+    // device to find block sizes)
+    {
+      const int nu = sp.upd_ptr[sp.nsup];
+      std::vector<int> ud(4 * std::max(nu, 1), 0), ur(std::max(nu, 1), 0);
+      std::vector<int> wbp(sp.nsup + 1, 0), wbe, cbp(sp.nsup + 1, 0), cbe;
+      const int wcap = dev::kKfWarpStage / 2, ccap = (kKsThreads / 32) * dev::kKfWarpStage - dev::kKfPosStage / 2;
+      for (idx t = 0; t < sp.nsup; ++t) {
+        auto batches = [&](int cap, std::vector<int>& ends, bool cta) {
+          int u = sp.upd_ptr[t];
+          while (u < sp.upd_ptr[t + 1]) {
+            int ue = u, used = 0, pused = 0;
+            while (ue < sp.upd_ptr[t + 1]) {
+              const int d = sp.upd_d[ue];
+              const int m = sp.sn_nrows[d] - sp.upd_off[ue], wd = sp.sn_first[d + 1] - sp.sn_first[d];
+              if (used + m * wd > cap || (cta && pused + m > dev::kKfPosStage)) break;
+              used += m * wd;
+              pused += m;
+              ++ue;
+            }
+            if (ue == u) ++ue;  // oversized block alone (applied from global memory)
+            ends.push_back(ue);
+            u = ue;
+          }
+        };
+        batches(wcap, wbe, false);
+        wbp[t + 1] = static_cast<int>(wbe.size());
+        batches(ccap, cbe, true);
+        cbp[t + 1] = static_cast<int>(cbe.size());
+      }
+      for (int u = 0; u < nu; ++u) {
+        const int d = sp.upd_d[u], o = sp.upd_off[u];
+        const int m = sp.sn_nrows[d] - o;
+        if (m >= (1 << 16) || sp.upd_cnt[u] >= (1 << 15)) throw InvalidArgument("supernode too tall for ks_factor");
+        ud[4 * u] = static_cast<int>(sp.sn_off[d] + o);
+        ud[4 * u + 1] = sp.sn_nrows[d];
+        ud[4 * u + 2] = m | (sp.upd_cnt[u] << 16);
+        ud[4 * u + 3] = sp.sn_first[d + 1] - sp.sn_first[d];
+        ur[u] = sp.sn_rows_ptr[d] + o;
+      }
+      ks.upd.upload(ud, st);
+      ks.upd_rows.upload(ur, st);
+      ks.wb_ptr.upload(wbp, st);
+      ks.wb_end.upload(wbe.empty() ? std::vector<int>{0} : wbe, st);
+      ks.cb_ptr.upload(cbp, st);
+      ks.cb_end.upload(cbe.empty() ? std::vector<int>{0} : cbe, st);
+    }
+    ks.lev_ptr.upload(lp, st);
+    ks.lev_sn.upload(ls.empty() ? std::vector<int>{0} : ls, st);
+    ks.wlev_ptr.upload(wp, st);
+    ks.wlev_sn.upload(ws.empty() ? std::vector<int>{0} : ws, st);
+    // [wide panel staging][per-warp staging areas]
+    ks.fsmem = (static_cast<std::size_t>(std::min<long long>(std::max<long long>(wide_max, 1), 12288)) +
+                static_cast<std::size_t>(kKsThreads / 32) * dev::kKfWarpStage) * 8;
+    CK(cudaFuncSetAttribute((const void*)dev::ks_factor<kKsThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(ks.fsmem)));
+    if (const char* e = std::getenv("HYKKT_KS_FACTOR")) ks.factor_on = std::atoi(e) ? 1 : 0;
+  }
   ks.smem = ks_smem_bytes(sp.n, nch, nch);
   CK(cudaFuncSetAttribute((const void*)dev::ks_solve<kKsThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(ks.smem)));
@@ -1143,12 +1224,58 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
   std::vector<int> act(Bp, 1), attempts(Bp, 0), fail(Bp, 0), failed_col(Bp, -1), ok(Bp, 0);
   const dev::SnPlan snp = c.snplan();
   const int nsrc = static_cast<int>(sp.src_to_panel.size());
+  const bool sysf = ks_prepare(c) && c.ks.factor_on;
+  if (sysf) {
+    // per-system contiguous H_gamma values for ks_factor
+    auto& ks = c.ks;
+    ks.hg.alloc(static_cast<std::size_t>(std::max<idx>(k.hg.nnz(), 1)) * B);
+    if (k.hg.nnz() > 0) {
+      dim3 grid(static_cast<unsigned>((k.hg.nnz() + 31) / 32), static_cast<unsigned>(Bp / 32));
+      dev::kb_deinterleave<<<grid, 256, 0, st>>>(bb.hg.p, ks.hg.p, static_cast<int>(k.hg.nnz()), B, Bp);
+      check_launch(c);
+    }
+  }
   for (int round = 0; round < 64; ++round) {
     bool any = false;
     for (int b = 0; b < Bp; ++b) any = any || act[b];
     if (!any) break;
     CK(cudaMemcpyAsync(bb.delta1.p, d1.data(), Bp * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(bb.active.p, act.data(), Bp * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (sysf) {
+      auto& ks = c.ks;
+      CK(cudaMemsetAsync(bb.fail.p, 0x7f, Bp * sizeof(int), st));
+      dev::KfArgs fa{};
+      fa.s = snp;
+      fa.panel_size = sp.panel_size;
+      fa.panel = bb.panel.p;
+      fa.hg = ks.hg.p;
+      fa.nsrc = nsrc;
+      fa.to_panel = c.src_to_panel.p;
+      fa.srow = c.src_row.p;
+      fa.scol = c.src_col.p;
+      fa.delta1 = bb.delta1.p;
+      fa.active = bb.active.p;
+      fa.maxdiag = bb.maxdiag.p;
+      fa.floor_rel = cfg.pivot_floor;
+      fa.fail_col = bb.fail.p;
+      fa.lev_ptr = ks.lev_ptr.p;
+      fa.lev_sn = ks.lev_sn.p;
+      fa.wlev_ptr = ks.wlev_ptr.p;
+      fa.wlev_sn = ks.wlev_sn.p;
+      fa.nlevels = sp.nlevels;
+      fa.smem_doubles = static_cast<int>(ks.fsmem / 8) - (kKsThreads / 32) * dev::kKfWarpStage;
+      fa.ticket = fresh_tickets(c, 1);
+      fa.B = B;
+      fa.upd = reinterpret_cast<const int4*>(ks.upd.p);
+      fa.upd_rows = ks.upd_rows.p;
+      fa.wb_ptr = ks.wb_ptr.p;
+      fa.wb_end = ks.wb_end.p;
+      fa.cb_ptr = ks.cb_ptr.p;
+      fa.cb_end = ks.cb_end.p;
+      const int grid = static_cast<int>(std::min<long long>(B, c.num_sms));
+      dev::ks_factor<kKsThreads><<<grid, kKsThreads, ks.fsmem, st>>>(fa);
+      check_launch(c);
+    } else {
     dev::kb_zero_panels<<<blocks_for(sp.panel_size * Bp), kThreads, 0, st>>>(sp.panel_size, bd, snp, bb.mode.p,
                                                                              bb.slot_sn.p, bb.active.p, bb.panel.p);
     check_launch(c);
@@ -1180,6 +1307,7 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     fa.njobs = bb.nfjobs;
     fa.smem_doubles = static_cast<int>(kBatchSmem / sizeof(double));
     if (sp.nsup > 0) coop_launch(c, (const void*)dev::kb_factor, c.coop_bfactor_blocks, &fa, kBatchSmem);
+    }
     CK(cudaMemcpyAsync(fail.data(), bb.fail.p, Bp * sizeof(int), cudaMemcpyDeviceToHost, st));
     read_status(c);
     for (int b = 0; b < Bp; ++b) {
@@ -1215,7 +1343,18 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     const SysPlan& P = ks.plan;
     const long long vlen = static_cast<long long>(P.src.size());
     ks.vals.alloc(static_cast<std::size_t>(B) * vlen);
-    {
+    if (sysf) {
+      ks.js.alloc(static_cast<std::size_t>(std::max<idx>(k.j.nnz(), 1)) * B);
+      if (k.j.nnz() > 0) {
+        dim3 grid(static_cast<unsigned>((k.j.nnz() + 31) / 32), static_cast<unsigned>(Bp / 32));
+        dev::kb_deinterleave<<<grid, 256, 0, st>>>(bb.js.p, ks.js.p, static_cast<int>(k.j.nnz()), B, Bp);
+        check_launch(c);
+      }
+      dim3 rg(static_cast<unsigned>((vlen + 255) / 256), static_cast<unsigned>(B));
+      dev::ks_remap_sys<<<rg, 256, 0, st>>>(ks.src.p, vlen, sp.panel_size, bb.panel.p, ks.js.p, k.j.nnz(),
+                                            ks.vals.p);
+      check_launch(c);
+    } else {
       dim3 rg(static_cast<unsigned>((vlen + 31) / 32), static_cast<unsigned>((B + 31) / 32));
       dev::ks_remap<<<rg, 256, 0, st>>>(ks.src.p, vlen, snp, bb.mode.p, bb.slot_sn.p, Bp, B, bb.panel.p, bb.js.p,
                                          ks.vals.p);

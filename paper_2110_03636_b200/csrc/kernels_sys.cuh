@@ -844,3 +844,356 @@ __global__ void ks_remap(const int* __restrict__ src, long long len, SnPlan s, c
 }
 
 }  // namespace hykkt::dev
+
+namespace hykkt::dev {
+
+// ---- system-per-CTA numeric factorization ---------------------------------
+// numeric_cholesky (proj/core/src/cholesky.cpp:65-137) for every system still
+// on the delta1 ladder (solver.cpp:108-142): one CTA per system at a time,
+// the system's panels contiguous in global memory (so the descendant blocks
+// it re-reads stay in L1/L2 while the CTA owns the system), supernodes in
+// level order with a CTA barrier per level: narrow supernodes are warp
+// tasks (left-looking updates from the descendant blocks, lanes over target
+// rows, then the dense factor of the panel), wide ones CTA tasks with the
+// panel staged in shared memory.  The pivot test is the reference's
+// !(pivot > floor) with floor = pivot_floor * max|diag H_gamma|
+// (solver.cpp:111); the first failing column is recorded with atomicMin.
+struct KfArgs {
+  SnPlan s;
+  long long panel_size;
+  double* panel;            // [B][panel_size]
+  const double* hg;         // [B][nsrc] H_gamma values (lower CSC order)
+  int nsrc;
+  const int* to_panel;      // nsrc -> panel slot
+  const int* srow;
+  const int* scol;
+  const double* delta1;     // [Bp]
+  const int* active;        // [Bp]
+  const double* maxdiag;    // [Bp]
+  double floor_rel;
+  int* fail_col;            // [Bp], INT_MAX on entry
+  const int* lev_ptr;       // nlevels + 1 (narrow list)
+  const int* lev_sn;        // narrow supernodes by level
+  const int* wlev_ptr;      // nlevels + 1 (wide list)
+  const int* wlev_sn;
+  int nlevels;
+  int smem_doubles;
+  unsigned* ticket;
+  int B;
+  // per update u (SupernodalPlan upd_* order): {panel offset of the block's
+  // first row (off[d] + upd_off), column stride nrows[d], rows m | cnt << 16,
+  // descendant width}, and the block's row list start (rows_ptr[d] + upd_off)
+  const int4* upd;
+  const int* upd_rows;
+  // per target supernode: staging batches of its update list (ends, in
+  // update index), for the warp capacity and the CTA capacity
+  const int* wb_ptr;   // nsup + 1 into wb_end
+  const int* wb_end;
+  const int* cb_ptr;
+  const int* cb_end;
+};
+
+extern __shared__ __align__(16) double kf_smem[];
+
+__device__ __forceinline__ void kf_dense_warp(double* P, int nr, int w, int f, double floor_v, int* fail, int lane) {
+  for (int k = 0; k < w; ++k) {
+    double* Pk = P + k * nr;
+    const double pivot = Pk[k];
+    if (!(pivot > floor_v) && lane == 0) atomicMin(fail, f + k);
+    const double dk = sqrt(pivot);
+    __syncwarp();
+    for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] / dk;
+    if (lane == 0) Pk[k] = dk;
+    __syncwarp();
+    for (int c = k + 1; c < w; ++c) {
+      const double lck = Pk[c];
+      double* Pc = P + c * nr;
+      for (int r = c + lane; r < nr; r += 32) Pc[r] = fma(-Pk[r], lck, Pc[r]);
+    }
+    __syncwarp();
+  }
+}
+
+// Per-warp staging area of ks_factor (doubles): a narrow target panel and
+// one descendant block at a time.
+constexpr int kKfWarpStage = 512;
+// CTA tasks: target positions of the staged block rows (ints), carved from
+// the end of the per-warp staging areas
+constexpr int kKfPosStage = 2048;
+
+// One left-looking update (cholesky.cpp:102-114 in supernodal form): target
+// entries of panel P (nr x w, columns f..) -= L_d[rows, :] L_d[jj rows, :]^T
+// for the cnt rows of descendant d that fall in the target's columns.  D =
+// the descendant block (m x wd, column stride ld) in shared or global memory.
+__device__ __forceinline__ void kf_apply(double* P, const int* R, int f, int w, int nr, const double* D, int ld,
+                                         int wd, int m, int cnt, const int* Rdo, int lane, int cmod, int cres) {
+  // row ii of the block (per lane): its target position is found once,
+  // then every column jj <= ii of the run is updated
+  for (int ii = lane; ii < m; ii += 32) {
+    const int r = __ldg(Rdo + ii);
+    const int pos = ii < cnt ? r - f : find_row(R, w, nr, r);
+    const int jmax = min(cnt, ii + 1);
+    for (int jj = 0; jj < jmax; ++jj) {
+      const int cc = __ldg(Rdo + jj) - f;
+      if (cmod > 1 && cc % cmod != cres) continue;
+      double d0 = 0.0, d1 = 0.0;
+      int k = 0;
+      for (; k + 2 <= wd; k += 2) {
+        d0 = fma(D[k * ld + ii], D[k * ld + jj], d0);
+        d1 = fma(D[(k + 1) * ld + ii], D[(k + 1) * ld + jj], d1);
+      }
+      if (k < wd) d0 = fma(D[k * ld + ii], D[k * ld + jj], d0);
+      P[cc * nr + pos] -= d0 + d1;
+    }
+  }
+}
+
+// All left-looking updates of target supernode sn, in update order, in
+// host-planned batches that fit the staging area (every load of a batch in
+// flight at once); a batch of one oversized block is applied straight from
+// global memory.  Warp version: lanes over the block rows.  CTA version:
+// warps over the block's target columns (each target entry owned by one
+// warp), the block rows' target positions staged once in shared memory.
+__device__ __forceinline__ void kf_updates_warp(const KfArgs& a, const double* Pb, int sn, double* P, const int* R,
+                                                int f, int w, int nr, double* stage, int cap, int lane) {
+  int u = a.s.upd_ptr[sn];
+  for (int bi = a.wb_ptr[sn], be = a.wb_ptr[sn + 1]; bi < be; ++bi) {
+    const int ue = __ldg(a.wb_end + bi);
+    int4 q = __ldg(a.upd + u);
+    if ((q.z & 0xffff) * q.w > cap) {  // oversized: direct
+      kf_apply(P, R, f, w, nr, Pb + q.x, q.y, q.w, q.z & 0xffff, q.z >> 16, a.s.rows + __ldg(a.upd_rows + u), lane, 1, 0);
+      __syncwarp();
+      u = ue;
+      continue;
+    }
+    int off = 0;
+    for (int v = u; v < ue; ++v) {
+      const int4 d = __ldg(a.upd + v);
+      const int m = d.z & 0xffff;
+      for (int e = lane; e < m * d.w; e += 32) {
+        const int k = e / m, ii = e - k * m;
+        stage[off + e] = Pb[d.x + k * d.y + ii];
+      }
+      off += m * d.w;
+    }
+    __syncwarp();
+    off = 0;
+    for (int v = u; v < ue; ++v) {
+      const int4 d = __ldg(a.upd + v);
+      const int m = d.z & 0xffff;
+      kf_apply(P, R, f, w, nr, stage + off, m, d.w, m, d.z >> 16, a.s.rows + __ldg(a.upd_rows + v), lane, 1, 0);
+      off += m * d.w;
+      __syncwarp();
+    }
+    u = ue;
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void kf_updates_cta(const KfArgs& a, const double* Pb, int sn, double* P, const int* R,
+                                               int f, int w, int nr, double* stage, int cap, int* pos_st) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = NT / 32;
+  int u = a.s.upd_ptr[sn];
+  for (int bi = a.cb_ptr[sn], be = a.cb_ptr[sn + 1]; bi < be; ++bi) {
+    const int ue = __ldg(a.cb_end + bi);
+    const int4 q0 = __ldg(a.upd + u);
+    const bool direct = (q0.z & 0xffff) * q0.w > cap;
+    // stage the blocks and their rows' target positions
+    int off = 0, poff = 0;
+    for (int v = u; v < ue; ++v) {
+      const int4 d = __ldg(a.upd + v);
+      const int m = d.z & 0xffff, cnt = d.z >> 16;
+      const int* Rdo = a.s.rows + __ldg(a.upd_rows + v);
+      if (!direct) {
+        for (int e = tid; e < m * d.w; e += NT) {
+          const int k = e / m, ii = e - k * m;
+          stage[off + e] = Pb[d.x + k * d.y + ii];
+        }
+      }
+      for (int ii = tid; ii < m; ii += NT) {
+        const int r = __ldg(Rdo + ii);
+        pos_st[poff + ii] = ii < cnt ? r - f : find_row(R, w, nr, r);
+      }
+      off += m * d.w;
+      poff += m;
+    }
+    __syncthreads();
+    off = 0;
+    poff = 0;
+    for (int v = u; v < ue; ++v) {
+      const int4 d = __ldg(a.upd + v);
+      const int m = d.z & 0xffff, cnt = d.z >> 16, wd = d.w;
+      const double* D = direct ? Pb + d.x : stage + off;
+      const int ld = direct ? d.y : m;
+      const int* Rdo = a.s.rows + __ldg(a.upd_rows + v);
+      // warps own target columns (cc mod NW): the updates of a batch are not
+      // separated by barriers, so a target column must stay with one warp
+      for (int jj = 0; jj < cnt; ++jj) {
+        const int cc = __ldg(Rdo + jj) - f;
+        if (cc % NW != wid) continue;
+        for (int ii = jj + lane; ii < m; ii += 32) {
+          double d0 = 0.0, d1 = 0.0;
+          int k = 0;
+          for (; k + 2 <= wd; k += 2) {
+            d0 = fma(D[k * ld + ii], D[k * ld + jj], d0);
+            d1 = fma(D[(k + 1) * ld + ii], D[(k + 1) * ld + jj], d1);
+          }
+          if (k < wd) d0 = fma(D[k * ld + ii], D[k * ld + jj], d0);
+          P[cc * nr + pos_st[poff + ii]] -= d0 + d1;
+        }
+      }
+      off += m * wd;
+      poff += m;
+    }
+    __syncthreads();
+    u = ue;
+  }
+}
+
+// warp task: narrow supernode sn (w nr <= kKfWarpStage / 2 is staged)
+__device__ void kf_warp_task(const KfArgs& a, double* Pb, int sn, double floor_v, int* fail, int lane, double* st) {
+  const SnPlan& s = a.s;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn], size = nr * w;
+  const int* R = s.rows + s.rows_ptr[sn];
+  double* Pg = Pb + s.off[sn];
+  const bool pst = size <= kKfWarpStage / 2;
+  double* P = pst ? st : Pg;
+  double* Dst = st + kKfWarpStage / 2;
+  if (pst) {
+    for (int e = lane; e < size; e += 32) P[e] = Pg[e];
+    __syncwarp();
+  }
+  kf_updates_warp(a, Pb, sn, P, R, f, w, nr, Dst, kKfWarpStage / 2, lane);
+  kf_dense_warp(P, nr, w, f, floor_v, fail, lane);
+  if (pst) {
+    for (int e = lane; e < size; e += 32) Pg[e] = P[e];
+    __syncwarp();
+  }
+}
+
+// CTA task: wide supernode; panel staged in shared memory when it fits,
+// each descendant block staged by the whole CTA (all loads in flight), warps
+// own target columns cc = wid (mod NW)
+template <int NT>
+__device__ void kf_cta_task(const KfArgs& a, double* Pb, int sn, double floor_v, int* fail, double* pan_st,
+                            double* blk_st, int blk_cap, int* pos_st) {
+  const SnPlan& s = a.s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = NT / 32;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn], size = nr * w;
+  const int* R = s.rows + s.rows_ptr[sn];
+  double* Pg = Pb + s.off[sn];
+  const bool fits = size <= a.smem_doubles;
+  double* P = fits ? pan_st : Pg;
+  if (fits) {
+    for (int e = tid; e < size; e += NT) P[e] = Pg[e];
+  }
+  __syncthreads();
+  kf_updates_cta<NT>(a, Pb, sn, P, R, f, w, nr, blk_st, blk_cap, pos_st);
+  // blocked right-looking factor: warp 0 factors 8 columns, all warps apply
+  // the rank-8 trailing update
+  constexpr int KB = 8;
+  for (int k0 = 0; k0 < w; k0 += KB) {
+    const int kb = min(KB, w - k0);
+    if (wid == 0) {
+      for (int k = k0; k < k0 + kb; ++k) {
+        double* Pk = P + k * nr;
+        const double pivot = Pk[k];
+        if (!(pivot > floor_v) && lane == 0) atomicMin(fail, f + k);
+        const double dk = sqrt(pivot);
+        __syncwarp();
+        for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] / dk;
+        if (lane == 0) Pk[k] = dk;
+        __syncwarp();
+        for (int c = k + 1; c < k0 + kb; ++c) {
+          const double lck = Pk[c];
+          double* Pc = P + c * nr;
+          for (int r = c + lane; r < nr; r += 32) Pc[r] = fma(-Pk[r], lck, Pc[r]);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int c = k0 + kb + wid; c < w; c += NW) {
+      double lc[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) lc[k] = k < kb ? P[(k0 + k) * nr + c] : 0.0;
+      double* Pc = P + c * nr;
+      for (int r = c + lane; r < nr; r += 32) {
+        double v = Pc[r];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+          if (k < kb) v = fma(-P[(k0 + k) * nr + r], lc[k], v);
+        }
+        Pc[r] = v;
+      }
+    }
+    __syncthreads();
+  }
+  if (fits) {
+    for (int e = tid; e < size; e += NT) Pg[e] = P[e];
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) ks_factor(KfArgs a) {
+  __shared__ int s_sys;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = NT / 32;
+  for (;;) {
+    if (tid == 0) s_sys = static_cast<int>(atomicAdd(a.ticket, 1u));
+    __syncthreads();
+    const int b = s_sys;
+    __syncthreads();
+    if (b >= a.B) break;
+    if (!a.active[b]) continue;
+    double* Pb = a.panel + static_cast<long long>(b) * a.panel_size;
+    const double* hg = a.hg + static_cast<long long>(b) * a.nsrc;
+    const double d1 = a.delta1[b];
+    for (long long i = tid; i < a.panel_size; i += NT) Pb[i] = 0.0;
+    __syncthreads();
+    for (int t = tid; t < a.nsrc; t += NT) {
+      double v = hg[t];
+      if (d1 != 0.0 && __ldg(a.srow + t) == __ldg(a.scol + t)) v = __dadd_rn(v, d1);
+      Pb[__ldg(a.to_panel + t)] = v;
+    }
+    __syncthreads();
+    const double floor_v = fmax(a.floor_rel * a.maxdiag[b], 0.0);
+    int* fail = a.fail_col + b;
+    // shared memory: [wide panel staging: smem_doubles][NW per-warp stages]
+    double* wst = kf_smem + a.smem_doubles;
+    for (int L = 0; L < a.nlevels; ++L) {
+      for (int i = a.lev_ptr[L] + wid; i < a.lev_ptr[L + 1]; i += NW)
+        kf_warp_task(a, Pb, a.lev_sn[i], floor_v, fail, lane, wst + wid * kKfWarpStage);
+      __syncthreads();
+      for (int i = a.wlev_ptr[L]; i < a.wlev_ptr[L + 1]; ++i)
+        kf_cta_task<NT>(a, Pb, a.wlev_sn[i], floor_v, fail, kf_smem, wst, NW * kKfWarpStage - kKfPosStage / 2,
+                        reinterpret_cast<int*>(wst + NW * kKfWarpStage - kKfPosStage / 2));
+      if (a.wlev_ptr[L + 1] > a.wlev_ptr[L]) __syncthreads();
+    }
+    __syncthreads();
+  }
+}
+
+// Value streams from per-system panels (ks_factor layout) and per-system
+// scaled J values: vals[b][e] (see sysplan_format.h source encoding).
+__global__ void ks_remap_sys(const int* __restrict__ src, long long len, long long panel_size,
+                             const double* __restrict__ panel, const double* __restrict__ js, long long nnz_j,
+                             double* __restrict__ vals) {
+  const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int b = blockIdx.y;
+  if (e >= len) return;
+  const int sc = __ldg(src + e);
+  double val = 0.0;
+  if (sc >= 0) {
+    val = panel[b * panel_size + (sc >> 1)];
+    if (sc & 1) val = 1.0 / val;
+  } else if (sc <= -2) {
+    val = js[b * nnz_j + (-2 - sc)];
+  }
+  vals[b * len + e] = val;
+}
+
+}  // namespace hykkt::dev
