@@ -442,12 +442,14 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
   //  0  cp.async: every thread copies its 16-byte slice of each chunk
   //     (LSU work spread over all warps; completion = one noinc arrival
   //     per copying thread on the chunk's mbarrier)
-  //  1  TMA: one bulk copy per chunk, issued by lane 0 of warp
+  //  1  TMA: one bulk copy per chunk, issued by producer lane
   //     (chunk mod issuers); bulk requests are accepted ~every 400 ns per
-  //     SM (tools/micro/tma_pure.cu), completion counted in bytes.
+  //     issuing thread (tools/micro/tma_pure.cu), completion counted in bytes.
   const int feed = a.feed;
-  const int issuers = min(a.issuers, NT / 32);
-  const bool issuer = lane == 0 && wid < issuers;
+  // TMA requests come from lanes of the producer warp only: compute warps
+  // carry no feed instructions
+  const int issuers = min(a.issuers, 32);
+  const bool issuer = producer && lane < issuers;
   const int vthr = (8 << vlg) / 16, ithr = (4 << ilg) / 16;  // cp.async copying threads per chunk
   const unsigned long long pol_v = policy_evict_first(), pol_i = policy_evict_last();
   auto issue_range = [&](long long v_from, long long v_to, long long i_from, long long i_to) {
@@ -471,14 +473,14 @@ __device__ __noinline__ void ks_run(const KsArgs& a, const KsSmem& S, const doub
       return;
     }
     if (!issuer) return;
-    for (long long gc = v_from + ((wid - v_from) % issuers + issuers) % issuers; gc < v_to; gc += issuers) {
+    for (long long gc = v_from + ((lane - v_from) % issuers + issuers) % issuers; gc < v_to; gc += issuers) {
       const long long c = cv0 + (gc - sv.G);
       const int slot = static_cast<int>(gc & (nvchunk - 1));
       unsigned long long* bar = barv + slot;
       mbar_expect_tx(bar, 8u << vlg);
       tma_load_1d(rv_s + (slot << vlg), vals + (c << vlg), 8u << vlg, bar, pol_v);
     }
-    for (long long gc = i_from + ((issuers - 1 - wid - i_from) % issuers + issuers) % issuers; gc < i_to;
+    for (long long gc = i_from + ((issuers - 1 - lane - i_from) % issuers + issuers) % issuers; gc < i_to;
          gc += issuers) {
       const long long c = ci0 + (gc - si.G);
       const int slot = static_cast<int>(gc & (nichunk - 1));
