@@ -290,14 +290,16 @@ __device__ __forceinline__ void ks_fwd_thread(const KsRing& R, double* v, const 
     double acc = v[f + r];
     if (inl) {
       const int c = R.I(ioff + r);
-      double a0 = 0.0, a1 = 0.0;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int k = 0;
-      for (; k + 2 <= c; k += 2) {
+      for (; k + 4 <= c; k += 4) {
         a0 = fma(R.V(e + k), v[R.I(ig + k)], a0);
         a1 = fma(R.V(e + k + 1), v[R.I(ig + k + 1)], a1);
+        a2 = fma(R.V(e + k + 2), v[R.I(ig + k + 2)], a2);
+        a3 = fma(R.V(e + k + 3), v[R.I(ig + k + 3)], a3);
       }
-      if (k < c) a0 = fma(R.V(e + k), v[R.I(ig + k)], a0);
-      acc -= a0 + a1;
+      for (; k < c; ++k) a0 = fma(R.V(e + k), v[R.I(ig + k)], a0);
+      acc -= (a0 + a1) + (a2 + a3);
       e += c;
       ig += c;
     } else {
@@ -316,14 +318,16 @@ __device__ __forceinline__ void ks_bwd_thread(const KsRing& R, double* v, const 
     const int cs = voff + k * w - k * (k - 1) / 2;
     double sk = 0.0;
     if (inl) {
-      double a1 = 0.0;
+      double a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int r = 0;
-      for (; r + 2 <= nb; r += 2) {
+      for (; r + 4 <= nb; r += 4) {
         sk = fma(R.V(e + r * w + k), v[R.I(ioff + 1 + r)], sk);
         a1 = fma(R.V(e + (r + 1) * w + k), v[R.I(ioff + 2 + r)], a1);
+        a2 = fma(R.V(e + (r + 2) * w + k), v[R.I(ioff + 3 + r)], a2);
+        a3 = fma(R.V(e + (r + 3) * w + k), v[R.I(ioff + 4 + r)], a3);
       }
-      if (r < nb) sk = fma(R.V(e + r * w + k), v[R.I(ioff + 1 + r)], sk);
-      sk += a1;
+      for (; r < nb; ++r) sk = fma(R.V(e + r * w + k), v[R.I(ioff + 1 + r)], sk);
+      sk += (a1 + a2) + a3;
     } else {
       for (int g = R.I(ioff + k), g1 = R.I(ioff + k + 1); g < g1; ++g) sk += part[g];
     }
