@@ -18,6 +18,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -106,6 +107,10 @@ struct hykkt_context {
   int num_sms = 0;
   int coop_factor_blocks = 0, coop_trsv_blocks = 0, coop_cg_blocks = 0, coop_ruiz_blocks = 0;
   int coop_bfactor_blocks = 0, coop_btrsv_blocks = 0, coop_bcg_blocks = 0, coop_bruiz_blocks = 0;
+  int coop_bruiz_rows_blocks = 0;
+  // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
+  hykkt::DBuf<int> ruiz_rp, ruiz_ent;
+  bool ruiz_rows_built = false;
 
   bool have_plan = false, have_kkt = false, have_values = false, have_factor = false;
   hykkt::SupernodalPlan sp;
@@ -310,6 +315,7 @@ void init_ctx(Ctx& c, int device) {
     c.coop_bcg_blocks = p2;
   }
   c.coop_bruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::kb_ruiz), 2 * c.num_sms);
+  c.coop_bruiz_rows_blocks = occupancy_blocks(c, (const void*)dev::kb_ruiz_rows);
   c.barrier.alloc(2);
   CK(cudaMemsetAsync(c.barrier.p, 0, 2 * sizeof(unsigned), c.stream));
   c.status.alloc(1);
@@ -368,6 +374,7 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   c.have_plan = true;
   c.bb.jobs_T = -1;
   c.ks.state = 0;
+  c.ruiz_rows_built = false;
   c.have_factor = false;
 }
 
@@ -1023,6 +1030,49 @@ std::size_t ks_smem_bytes(idx n, int nv, int ni) {
 // solve vector.  Infeasible (the lane-per-system kernels are used) when not
 // even 4-chunk rings fit or a supernode block does not fit the rings;
 // HYKKT_BATCH_PATH=lane forces the lane path.
+// Row lists for kb_ruiz_rows: every stored entry of H_tilde (CSC, lower)
+// appears in the list of its row and, off the diagonal, of its column; every
+// J entry (CSC) in the list of constraint row n_x + k and of column j.
+void ruiz_rows_prepare(Ctx& c) {
+  if (c.ruiz_rows_built) return;
+  const KktPlan& k = c.kp;
+  const idx nrow = k.nx + k.mc, nht = k.ht.nnz();
+  std::vector<int> cnt(nrow + 1, 0);
+  for (idx col = 0; col < k.nx; ++col) {
+    for (idx t = k.ht.cp[col]; t < k.ht.cp[col + 1]; ++t) {
+      cnt[k.ht.ri[t] + 1]++;
+      if (k.ht.ri[t] != col) cnt[col + 1]++;
+    }
+    for (idx q = k.j.cp[col]; q < k.j.cp[col + 1]; ++q) {
+      cnt[k.nx + k.j.ri[q] + 1]++;
+      cnt[col + 1]++;
+    }
+  }
+  std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+  std::vector<int> ent(4 * std::max<idx>(cnt[nrow], 1), 0), cur(cnt.begin(), cnt.end() - 1);
+  auto put = [&](idx r, idx vi, idx da, idx db) {
+    const int e = cur[r]++;
+    ent[4 * e] = static_cast<int>(vi);
+    ent[4 * e + 1] = static_cast<int>(da);
+    ent[4 * e + 2] = static_cast<int>(db);
+  };
+  for (idx col = 0; col < k.nx; ++col) {
+    for (idx t = k.ht.cp[col]; t < k.ht.cp[col + 1]; ++t) {
+      const idx row = k.ht.ri[t];
+      put(row, t, row, col);
+      if (row != col) put(col, t, row, col);
+    }
+    for (idx q = k.j.cp[col]; q < k.j.cp[col + 1]; ++q) {
+      const idx r = k.nx + k.j.ri[q];
+      put(r, nht + q, r, col);
+      put(col, nht + q, r, col);
+    }
+  }
+  c.ruiz_rp.upload(cnt, c.stream);
+  c.ruiz_ent.upload(ent, c.stream);
+  c.ruiz_rows_built = true;
+}
+
 bool ks_prepare(Ctx& c) {
   auto& ks = c.ks;
   if (ks.state != 0) return ks.state == 1;
@@ -1059,6 +1109,7 @@ bool ks_prepare(Ctx& c) {
   cudaStream_t st = c.stream;
   ks.idx.upload(ks.plan.idx, st);
   ks.src.upload(ks.plan.src, st);
+
   {
     // ks_factor level lists: wide supernodes (CTA tasks) vs narrow (warp tasks)
     std::vector<int> lp(sp.nlevels + 1, 0), wp(sp.nlevels + 1, 0), ls, ws;
@@ -1208,7 +1259,17 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     ra.tol = cfg.ruiz_tol;
     ra.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
     ra.abort = abort;
-    coop_launch(c, (const void*)dev::kb_ruiz, c.coop_bruiz_blocks, &ra);
+    static const bool atomics = [] {
+      const char* e = std::getenv("HYKKT_RUIZ_ATOMIC");
+      return e && std::atoi(e) != 0;
+    }();
+    if (!atomics) {
+      ruiz_rows_prepare(c);
+      dev::BRuizRowsArgs rr{ra, c.ruiz_rp.p, reinterpret_cast<const int4*>(c.ruiz_ent.p)};
+      coop_launch(c, (const void*)dev::kb_ruiz_rows, c.coop_bruiz_rows_blocks, &rr);
+    } else {
+      coop_launch(c, (const void*)dev::kb_ruiz, c.coop_bruiz_blocks, &ra);
+    }
   }
   dev::kb_scale<<<grid_of(std::max<idx>({k.ht.nnz(), k.j.nnz(), nx, mc})), kThreads, 0, st>>>(
       ap, bd, bb.d.p, bb.ht.p, v.j, bb.rx.p, v.ry, bb.hts.p, bb.js.p, bb.jscsr.p, bb.rxs.p, bb.rys.p);

@@ -192,6 +192,62 @@ __global__ void kb_ruiz(BRuizArgs a) {
   }
 }
 
+// ruiz_scale (ruiz.cpp:76-116) for every system in lockstep, by ROW
+// GATHERS instead of atomics: thread (row i, system b) — lanes are systems,
+// so every load is coalesced over the interleaved layout — takes the max of
+// the scaled magnitudes of row i of [[H_tilde, J^T], [J, 0]] from a host-built
+// row list (rp / ent: value index, ht slot or n_ht + J entry, and the entry's
+// stored row and column).  Each magnitude is formed exactly as kb_ruiz and
+// the reference do ((|a| d_row) d_col), and max is order-free, so d and the
+// sweep counts are bit-identical to kb_ruiz; two grid barriers per sweep.
+struct BRuizRowsArgs {
+  BRuizArgs r;
+  const int* rp;    // n_x + m_c + 1
+  const int4* ent;  // {value index, d row, d col, 0}
+};
+
+__global__ void kb_ruiz_rows(BRuizRowsArgs ar) {
+  const BRuizArgs& a = ar.r;
+  const int Bp = a.bd.Bp, nht = a.p.n_ht;
+  const long long nrow = (long long)(a.p.nx + a.p.mc) * Bp;
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  for (long long i = gt; i < nrow; i += gs) a.d[i] = 1.0;
+  for (long long b = gt; b < Bp; b += gs) a.sweeps[b] = a.max_iters;
+  grid_sync(a.bar, a.abort);
+  for (int it = 1; it <= a.max_iters; ++it) {
+    const int* prev = a.unconverged + (it - 1) * Bp;
+    int* cur = a.unconverged + it * Bp;
+    for (long long g = gt; g < nrow; g += gs) {
+      const int b = static_cast<int>(g % Bp);
+      if (it > 1 && !ldcg_int(prev + b)) continue;
+      const int i = static_cast<int>(g / Bp);
+      double nm = 0.0;
+      for (int e = __ldg(ar.rp + i), e1 = __ldg(ar.rp + i + 1); e < e1; ++e) {
+        const int4 q = __ldg(ar.ent + e);
+        const double av = q.x < nht ? a.ht[bidx(q.x, Bp, b)] : a.jval[bidx(q.x - nht, Bp, b)];
+        nm = fmax(nm, __dmul_rn(__dmul_rn(fabs(av), ldcg(a.d + bidx(q.y, Bp, b))), ldcg(a.d + bidx(q.z, Bp, b))));
+      }
+      a.norms[g] = nm;
+      if (nm > 0.0 && fabs(nm - 1.0) > a.tol) cur[b] = 1;
+    }
+    grid_sync(a.bar, a.abort);
+    for (long long b = gt; b < Bp; b += gs) {
+      const bool was_active = it == 1 || ldcg_int(prev + b);
+      if (was_active && !ldcg_int(cur + b)) a.sweeps[b] = it;
+      if (ldcg_int(cur + b)) atomicAdd(a.active_count + it, 1);
+    }
+    for (long long g = gt; g < nrow; g += gs) {
+      const int b = static_cast<int>(g % Bp);
+      if (!ldcg_int(cur + b)) continue;
+      const double v = ldcg(a.norms + g);
+      if (v > 0.0) a.d[g] = __ddiv_rn(ldcg(a.d + g), __dsqrt_rn(v));
+    }
+    grid_sync(a.bar, a.abort);
+    if (ldcg_int(a.active_count + it) == 0) break;
+  }
+}
+
 __global__ void kb_scale(AsmPlan p, BDims bd, const double* __restrict__ d, const double* __restrict__ ht,
                          const double* __restrict__ jval, const double* __restrict__ r_x,
                          const double* __restrict__ r_y, double* __restrict__ hts, double* __restrict__ js,
