@@ -29,6 +29,7 @@
 #include "kernels_solve.cuh"
 #include "kernels_batch.cuh"
 #include "kernels_sys.cuh"
+#include "kernels_mf.cuh"
 #include "sysplan.hpp"
 
 namespace hykkt {
@@ -107,7 +108,13 @@ struct hykkt_context {
   int num_sms = 0;
   int coop_factor_blocks = 0, coop_trsv_blocks = 0, coop_cg_blocks = 0, coop_ruiz_blocks = 0;
   int coop_bfactor_blocks = 0, coop_btrsv_blocks = 0, coop_bcg_blocks = 0, coop_bruiz_blocks = 0;
-  int coop_bruiz_rows_blocks = 0;
+  int coop_bruiz_rows_blocks = 0, coop_mf_blocks = 0;
+  // multifrontal single-system factor (kernels_mf.cuh)
+  hykkt::DBuf<long long> mf_uoff;
+  hykkt::DBuf<int> mf_task_ptr, mf_task_sn;
+  hykkt::DBuf<unsigned char> mf_task_big;
+  hykkt::DBuf<double> mf_ubuf;
+  int mf_ntasks = 0, mf_on = 1;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
   bool ruiz_rows_built = false;
@@ -302,6 +309,7 @@ void init_ctx(Ctx& c, int device) {
   CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
   if (!coop) throw CudaError("device does not support cooperative launch");
   c.coop_factor_blocks = occupancy_blocks(c, (const void*)dev::k_factor);
+  c.coop_mf_blocks = occupancy_blocks(c, (const void*)dev::k_mf_factor);
   c.coop_trsv_blocks = occupancy_blocks(c, (const void*)dev::k_trsv);
   c.coop_cg_blocks = occupancy_blocks(c, (const void*)dev::k_cg);
   c.coop_ruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_ruiz), 2 * c.num_sms);
@@ -369,6 +377,47 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   c.bvec.alloc(s.n);
   c.xvec.alloc(s.n);
   c.fac_done.alloc(s.nsup);
+  {
+    // multifrontal factor: update-matrix offsets and the level-ordered task
+    // list (one wide supernode per CTA task, up to 8 narrow ones of a level
+    // per warp-group task)
+    int big_rows = 64;
+    if (const char* e = std::getenv("HYKKT_MF_BIG")) big_rows = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("HYKKT_FACTOR")) c.mf_on = std::string(e) != "ll";
+    std::vector<long long> uo(s.nsup + 1, 0);
+    for (idx k = 0; k < s.nsup; ++k) {
+      const long long m = s.sn_nrows[k] - (s.sn_first[k + 1] - s.sn_first[k]);
+      uo[k + 1] = uo[k] + m * m;
+    }
+    std::vector<int> tp{0}, tsn;
+    std::vector<unsigned char> tbig;
+    idx q = 0;
+    while (q < s.nsup) {
+      const int lev = s.sn_level[s.order[q]];
+      std::vector<int> narrow;
+      for (; q < s.nsup && s.sn_level[s.order[q]] == lev; ++q) {
+        const int sn = s.order[q];
+        if (s.sn_nrows[sn] >= big_rows) {
+          tsn.push_back(sn);
+          tp.push_back(static_cast<int>(tsn.size()));
+          tbig.push_back(1);
+        } else {
+          narrow.push_back(sn);
+        }
+      }
+      for (std::size_t g = 0; g < narrow.size(); g += kThreads / 32) {
+        for (std::size_t h = g; h < std::min(narrow.size(), g + kThreads / 32); ++h) tsn.push_back(narrow[h]);
+        tp.push_back(static_cast<int>(tsn.size()));
+        tbig.push_back(0);
+      }
+    }
+    c.mf_uoff.upload(uo, st);
+    c.mf_task_ptr.upload(tp, st);
+    c.mf_task_sn.upload(tsn.empty() ? std::vector<int>{0} : tsn, st);
+    c.mf_task_big.upload(tbig.empty() ? std::vector<unsigned char>{0} : tbig, st);
+    c.mf_ntasks = static_cast<int>(tbig.size());
+    c.mf_ubuf.alloc(static_cast<std::size_t>(std::max<long long>(1, uo.back())));
+  }
   CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   c.epoch = 0;
   c.have_plan = true;
@@ -425,7 +474,28 @@ int factor_attempt(Ctx& c, const double* src, double delta1, double floor_abs,
   fa.fail_col = &c.status.p->fail_col;
   fa.abort = &c.status.p->abort;
   fa.ticket = fresh_tickets(c, 1);
-  if (s.nsup > 0) coop_launch(c, (const void*)dev::k_factor, c.coop_factor_blocks, &fa);
+  if (s.nsup > 0 && c.mf_on) {
+    dev::MfArgs ma;
+    ma.s = fa.s;
+    ma.panel = c.panel.p;
+    ma.ubuf = c.mf_ubuf.p;
+    ma.uoff = c.mf_uoff.p;
+    ma.task_ptr = c.mf_task_ptr.p;
+    ma.task_sn = c.mf_task_sn.p;
+    ma.task_big = c.mf_task_big.p;
+    ma.ntasks = c.mf_ntasks;
+    ma.done = fa.done;
+    ma.epoch = fa.epoch;
+    ma.floor_abs = floor_abs;
+    ma.maxdiag = maxdiag;
+    ma.floor_rel = floor_rel;
+    ma.fail_col = fa.fail_col;
+    ma.abort = fa.abort;
+    ma.ticket = fa.ticket;
+    coop_launch(c, (const void*)dev::k_mf_factor, c.coop_mf_blocks, &ma);
+  } else if (s.nsup > 0) {
+    coop_launch(c, (const void*)dev::k_factor, c.coop_factor_blocks, &fa);
+  }
   const StatusBlock sb = read_status(c);
   const int failed = sb.fail_col >= static_cast<int>(s.n) ? -1 : sb.fail_col;
   if (std::getenv("HYKKT_DEBUG")) std::fprintf(stderr, "[hykkt] factor attempt delta1=%g failed=%d\n", delta1, failed);

@@ -44,3 +44,19 @@ for k in range(ns):
         print(f"{k:4d} {steps[k][0]} {steps[k][2]:5d} {steps[k][1]:5d} | issue {rel[:,1].max():5d} hdr {rel[:,2].max():5d} "
               f"arrive min {arrive.min():5d} med {int(np.median(arrive)):5d} max {arrive.max():6d} (warp {last:2d}) next {nxt:6d}")
 print("sums over steps (us): max issue %.1f, max header %.1f, max arrive %.1f, step span %.1f" % tuple(tot / 1e3))
+# producer-bound steps: how much the step would shrink if the producer
+# arrived with the slowest compute warp
+ex, cnt, comp = 0, 0, 0
+for k in range(ns):
+    if w[k, 0, 0] == 0:
+        continue
+    t0 = w[k, :, 0].min()
+    rel = w[k] - t0
+    pc = rel[15, 4]
+    cm = rel[:15, 4].max()
+    comp += cm
+    if pc > cm:
+        ex += pc - cm
+        cnt += 1
+print("producer last in %d steps; excess %.1f us; compute-only arrive sum %.1f us; compute issue-wait sum %.1f us" % (
+    cnt, ex / 1e3, comp / 1e3, sum((w[k, :15, 1] - w[k, :, 0].min()).max() for k in range(ns) if w[k, 0, 0]) / 1e3))
