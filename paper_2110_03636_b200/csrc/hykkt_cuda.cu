@@ -115,6 +115,10 @@ struct hykkt_context {
   hykkt::DBuf<unsigned char> mf_task_big;
   hykkt::DBuf<double> mf_ubuf;
   int mf_ntasks = 0, mf_on = 1;
+  // single-system triangular-solve CTA tasks (kernels_solve.cuh trsv_pass)
+  hykkt::DBuf<int> tr_task_ptr, tr_task_sn, tr_pos;
+  hykkt::DBuf<unsigned char> tr_task_big;
+  int tr_ntasks = 0;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
   bool ruiz_rows_built = false;
@@ -330,6 +334,37 @@ void init_ctx(Ctx& c, int device) {
   CK(cudaMemsetAsync(c.status.p, 0, sizeof(StatusBlock), c.stream));
 }
 
+// Level-ordered CTA task list: supernodes with big(sn) are single-supernode
+// (whole CTA) tasks, the others are grouped per level, up to one per warp.
+template <class Pred>
+void level_tasks(const SupernodalPlan& s, Pred big, std::vector<int>& tp, std::vector<int>& tsn,
+                 std::vector<unsigned char>& tbig) {
+  tp.assign(1, 0);
+  tsn.clear();
+  tbig.clear();
+  idx q = 0;
+  while (q < s.nsup) {
+    const int lev = s.sn_level[s.order[q]];
+    std::vector<int> narrow;
+    for (; q < s.nsup && s.sn_level[s.order[q]] == lev; ++q) {
+      const int sn = s.order[q];
+      if (big(sn)) {
+        tsn.push_back(sn);
+        tp.push_back(static_cast<int>(tsn.size()));
+        tbig.push_back(1);
+      } else {
+        narrow.push_back(sn);
+      }
+    }
+    for (std::size_t g = 0; g < narrow.size(); g += kThreads / 32) {
+      for (std::size_t h = g; h < std::min(narrow.size(), g + kThreads / 32); ++h) tsn.push_back(narrow[h]);
+      tp.push_back(static_cast<int>(tsn.size()));
+      tbig.push_back(0);
+    }
+  }
+}
+
+
 void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   const SupernodalPlan& s = c.sp;
   cudaStream_t st = c.stream;
@@ -389,34 +424,33 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
       const long long m = s.sn_nrows[k] - (s.sn_first[k + 1] - s.sn_first[k]);
       uo[k + 1] = uo[k] + m * m;
     }
-    std::vector<int> tp{0}, tsn;
+    std::vector<int> tp, tsn;
     std::vector<unsigned char> tbig;
-    idx q = 0;
-    while (q < s.nsup) {
-      const int lev = s.sn_level[s.order[q]];
-      std::vector<int> narrow;
-      for (; q < s.nsup && s.sn_level[s.order[q]] == lev; ++q) {
-        const int sn = s.order[q];
-        if (s.sn_nrows[sn] >= big_rows) {
-          tsn.push_back(sn);
-          tp.push_back(static_cast<int>(tsn.size()));
-          tbig.push_back(1);
-        } else {
-          narrow.push_back(sn);
-        }
-      }
-      for (std::size_t g = 0; g < narrow.size(); g += kThreads / 32) {
-        for (std::size_t h = g; h < std::min(narrow.size(), g + kThreads / 32); ++h) tsn.push_back(narrow[h]);
-        tp.push_back(static_cast<int>(tsn.size()));
-        tbig.push_back(0);
-      }
-    }
+    level_tasks(s, [&](int sn) { return s.sn_nrows[sn] >= big_rows; }, tp, tsn, tbig);
     c.mf_uoff.upload(uo, st);
     c.mf_task_ptr.upload(tp, st);
     c.mf_task_sn.upload(tsn.empty() ? std::vector<int>{0} : tsn, st);
     c.mf_task_big.upload(tbig.empty() ? std::vector<unsigned char>{0} : tbig, st);
     c.mf_ntasks = static_cast<int>(tbig.size());
     c.mf_ubuf.alloc(static_cast<std::size_t>(std::max<long long>(1, uo.back())));
+  }
+  {
+    // triangular-solve task list: wide supernodes (panel >= HYKKT_TRSV_WIDE
+    // entries, rows within the shared staging buffer) as CTA tasks
+    long long wide = 2048;
+    if (const char* e = std::getenv("HYKKT_TRSV_WIDE")) wide = std::max(1ll, std::atoll(e));
+    std::vector<int> tp, tsn, pos(std::max<idx>(1, s.nsup));
+    std::vector<unsigned char> tbig;
+    level_tasks(s, [&](int sn) {
+      const long long w = s.sn_first[sn + 1] - s.sn_first[sn];
+      return s.sn_nrows[sn] <= dev::kWideMaxRows && w * s.sn_nrows[sn] >= wide;
+    }, tp, tsn, tbig);
+    for (idx k = 0; k < s.nsup; ++k) pos[s.order[k]] = static_cast<int>(k);
+    c.tr_task_ptr.upload(tp, st);
+    c.tr_task_sn.upload(tsn.empty() ? std::vector<int>{0} : tsn, st);
+    c.tr_task_big.upload(tbig.empty() ? std::vector<unsigned char>{0} : tbig, st);
+    c.tr_pos.upload(pos, st);
+    c.tr_ntasks = static_cast<int>(tbig.size());
   }
   CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   c.epoch = 0;
@@ -519,6 +553,11 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.rhs.jval = nullptr;
   ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
   ta.trace = nullptr;
+  ta.task_ptr = c.tr_task_ptr.p;
+  ta.task_sn = c.tr_task_sn.p;
+  ta.task_big = c.tr_task_big.p;
+  ta.ntasks = c.tr_ntasks;
+  ta.pos = c.tr_pos.p;
   return ta;
 }
 

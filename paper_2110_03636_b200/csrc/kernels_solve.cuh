@@ -75,6 +75,20 @@ struct TrsvArgs {
   GridBarrier bar;
   unsigned* ticket;           // task counter of this pass (zero on entry)
   unsigned long long* trace;  // diagnostics: per-task end / start times (ns)
+  // CTA task list in level order (forward; backward runs it reversed): one
+  // wide supernode per task (whole CTA) or up to 8 narrow ones (one per warp)
+  const int* task_ptr;
+  const int* task_sn;
+  const unsigned char* task_big;
+  int ntasks;
+  const int* pos;             // supernode -> position in s.order (trace slots)
+};
+
+constexpr int kWideMaxRows = 2048;  // wide (CTA) solve tasks stage nrows doubles in shared memory
+struct TrsvSmem {
+  double a[kWideMaxRows];
+  double t[32];
+  int task, first, count, big;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -335,19 +349,182 @@ __device__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
   }
 }
 
-// One forward + backward pass; y and x must hold kUnset on entry.
-__device__ __forceinline__ void trsv_pass(const TrsvArgs& a) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int ns = a.s.nsup;
-  (void)gw;
-  (void)nw;
-  for (long long t = grab_task(a.ticket, lane); t < 2 * ns; t = grab_task(a.ticket, lane)) {
-    if (a.trace && lane == 0) a.trace[2 * ns + t] = global_ns();
-    if (t < ns) fwd_task(a, a.s.order[t], lane, t);
-    else bwd_task(a, a.s.order[2 * ns - 1 - t], lane, t);
-    if (a.trace && lane == 0) a.trace[t] = global_ns();
+// Wide supernode, forward, whole CTA (multifrontal form as fwd_task):
+// A (shared) = b - children's contributions for own rows, running update for
+// rows below; per 32-column chunk warp 0 solves the diagonal block (shuffle
+// chain, reciprocal of the diagonal off the chain), then one thread per row
+// applies the chunk to the rows below with all 32 panel loads in flight.
+__device__ void fwd_cta(const TrsvArgs& a, TrsvSmem& S, int sn) {
+  const SnPlan& s = a.s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const double* P = a.panel + s.off[sn];
+  double* U = a.u + s.u_off[sn];
+  double* A = S.a;
+  for (int q = tid; q < nr; q += blockDim.x) A[q] = q < w ? rhs_at(a, f + q) : 0.0;
+  for (int c = s.child_ptr[sn] + tid; c < s.child_ptr[sn + 1]; c += blockDim.x) {
+    const int ch = s.child[c];
+    poll_value(a.u + s.u_off[ch + 1] - 1, a.abort);
+  }
+  __syncthreads();
+  for (int c = s.child_ptr[sn]; c < s.child_ptr[sn + 1]; ++c) {
+    const int ch = s.child[c];
+    const int m = s.nrows[ch] - (s.first[ch + 1] - s.first[ch]);
+    const double* uc = a.u + s.u_off[ch];
+    const int* rel = s.relind + s.u_off[ch];
+    for (int t = tid; t < m; t += blockDim.x) {
+      const int q = __ldg(rel + t);
+      const double v = load_ready(uc + t, a.abort);
+      A[q] += (q < w) ? -v : v;
+    }
+    __syncthreads();
+  }
+  for (int cb = 0; cb < w; cb += 32) {
+    const int cw = min(32, w - cb);
+    if (wid == 0) {
+      const int rl = cb + min(lane, cw - 1);
+      double d[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[k] = __ldg(P + (cb + min(k, cw - 1)) * nr + rl);
+      const double rd = 1.0 / __ldg(P + rl * nr + rl);
+      double acc = lane < cw ? A[cb + lane] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k < cw) {
+          const double yk = __shfl_sync(0xffffffffu, acc, k) * __shfl_sync(0xffffffffu, rd, k);
+          if (lane == k) acc = yk;
+          if (lane > k && lane < cw) acc = fma(-d[k], yk, acc);
+        }
+      }
+      if (lane < cw) {
+        A[cb + lane] = acc;
+        stcg(a.y + f + cb + lane, acc);
+      }
+    }
+    __syncthreads();
+    for (int q = cb + cw + tid; q < nr; q += blockDim.x) {
+      double l[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) l[k] = __ldg(P + (cb + min(k, cw - 1)) * nr + q);
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k < cw) t = fma(l[k], A[cb + k], t);
+      }
+      A[q] += (q < w) ? -t : t;
+    }
+    __syncthreads();
+  }
+  for (int q = w + tid; q < nr; q += blockDim.x) stcg(U + q - w, A[q]);
+}
+
+// Wide supernode, backward, whole CTA: X (shared) holds the solution at the
+// panel's rows; per chunk (last first) the below-chunk dot products are split
+// over 8 row slices per column and combined in a fixed order, then warp 0
+// runs the backward chain of the diagonal block.  The first chunk (holding
+// the supernode's first column, which children poll) is written last.
+__device__ void bwd_cta(const TrsvArgs& a, TrsvSmem& S, int sn) {
+  const SnPlan& s = a.s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const double* P = a.panel + s.off[sn];
+  const int* R = s.rows + s.rows_ptr[sn];
+  double* X = S.a;
+  const int par = s.parent[sn];
+  if (tid == 0) poll_value(par >= 0 ? a.x + s.first[par] : a.y + f, a.abort);
+  __syncthreads();
+  for (int r = w + tid; r < nr; r += blockDim.x) X[r] = load_ready(a.x + __ldg(R + r), a.abort);
+  __syncthreads();
+  const int nchunks = (w + 31) >> 5;
+  const int col = tid >> 3, slice = tid & 7;  // 32 columns x 8 row slices
+  for (int ci = nchunks - 1; ci >= 0; --ci) {
+    const int cb = ci * 32, cw = min(32, w - cb), rb0 = cb + cw;
+    double t = 0.0;
+    if (col < cw) {
+      const double* Pc = P + (cb + col) * nr;
+      int r = rb0 + slice;
+      for (; r + 24 < nr; r += 32) {
+        t = fma(__ldg(Pc + r), X[r], t);
+        t = fma(__ldg(Pc + r + 8), X[r + 8], t);
+        t = fma(__ldg(Pc + r + 16), X[r + 16], t);
+        t = fma(__ldg(Pc + r + 24), X[r + 24], t);
+      }
+      for (; r < nr; r += 8) t = fma(__ldg(Pc + r), X[r], t);
+    }
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 4);
+    if (slice == 0) S.t[col] = t;
+    __syncthreads();
+    if (wid == 0) {
+      const int cl = cb + min(lane, cw - 1);
+      double d[32];  // L(cb+k, cb+lane)
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[k] = __ldg(P + cl * nr + cb + min(k, cw - 1));
+      const double rd = 1.0 / __ldg(P + cl * nr + cl);
+      double acc = lane < cw ? load_ready(a.y + f + cb + lane, a.abort) - S.t[lane] : 0.0;
+#pragma unroll
+      for (int k = 31; k >= 0; --k) {
+        if (k < cw) {
+          const double xk = __shfl_sync(0xffffffffu, acc, k) * __shfl_sync(0xffffffffu, rd, k);
+          if (lane == k) acc = xk;
+          if (lane < k) acc = fma(-d[k], xk, acc);
+        }
+      }
+      if (lane < cw) {
+        X[cb + lane] = acc;
+        if (lane > 0 || ci > 0) stcg(a.x + f + cb + lane, acc);
+        if (a.x_out) a.x_out[s.perm[f + cb + lane]] = acc;
+      }
+      if (ci == 0) {
+        __syncwarp();
+        if (lane == 0) {
+          fence_gpu();
+          stcg(a.x + f, acc);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// One forward + backward pass; y and x must hold kUnset on entry.  CTAs
+// take tasks in order from the ticket (forward tasks in level order, then
+// the same list reversed for the backward pass).
+__device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nt = a.ntasks, ns = a.s.nsup;
+  for (;;) {
+    if (tid == 0) {
+      const int t = static_cast<int>(atomicAdd(a.ticket, 1u));
+      S.task = t;
+      if (t < 2 * nt) {
+        const int ti = t < nt ? t : 2 * nt - 1 - t;
+        S.first = a.task_ptr[ti];
+        S.count = a.task_ptr[ti + 1] - a.task_ptr[ti];
+        S.big = a.task_big[ti];
+      }
+    }
+    __syncthreads();
+    const int t = S.task;
+    if (t >= 2 * nt) break;
+    const bool fwd = t < nt;
+    if (S.big) {
+      const int sn = a.task_sn[S.first];
+      const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
+      if (a.trace && tid == 0) a.trace[2 * ns + slot] = global_ns();
+      if (fwd) fwd_cta(a, S, sn);
+      else bwd_cta(a, S, sn);
+      if (a.trace && tid == 0) a.trace[slot] = global_ns();
+    } else if (wid < S.count) {
+      const int sn = a.task_sn[S.first + wid];
+      const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
+      if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
+      if (fwd) fwd_task(a, sn, lane, slot);
+      else bwd_task(a, sn, lane, slot);
+      if (a.trace && lane == 0) a.trace[slot] = global_ns();
+    }
+    __syncthreads();
   }
 }
 
@@ -358,9 +535,10 @@ __device__ __forceinline__ void rearm(const TrsvArgs& a) {
 }
 
 __global__ void __launch_bounds__(256) k_trsv(TrsvArgs a) {
+  __shared__ TrsvSmem S;
   rearm(a);
   grid_sync(a.bar, a.abort);
-  trsv_pass(a);
+  trsv_pass(a, S);
 }
 
 // L values in forward row-list order (after a successful factorization).
@@ -428,6 +606,7 @@ __device__ __forceinline__ double reduce_partials(const double* partials, int sl
 
 __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
   __shared__ double scratch[33];
+  __shared__ TrsvSmem S;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int gs = gridDim.x * blockDim.x;
   int* abort = a.tr.abort;
@@ -455,7 +634,7 @@ __global__ void __launch_bounds__(256) k_cg(CgArgs a) {
   TrsvArgs tr = a.tr;
   for (long long it = 1; it <= a.max_iter; ++it) {
     tr.ticket = a.tickets + it;
-    trsv_pass(tr);
+    trsv_pass(tr, S);
     grid_sync(bar, abort);
     double pq = 0.0, pp = 0.0;
     for (int k = gt; k < a.mc; k += gs) {
