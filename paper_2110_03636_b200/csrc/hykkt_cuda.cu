@@ -109,6 +109,7 @@ struct hykkt_context {
   int coop_factor_blocks = 0, coop_trsv_blocks = 0, coop_cg_blocks = 0, coop_ruiz_blocks = 0;
   int coop_bfactor_blocks = 0, coop_btrsv_blocks = 0, coop_bcg_blocks = 0, coop_bruiz_blocks = 0;
   int coop_bruiz_rows_blocks = 0, coop_mf_blocks = 0;
+  const void* cg_fn = nullptr;
   // multifrontal single-system factor (kernels_mf.cuh)
   hykkt::DBuf<long long> mf_uoff;
   hykkt::DBuf<int> mf_task_ptr, mf_task_sn;
@@ -118,7 +119,8 @@ struct hykkt_context {
   // single-system triangular-solve CTA tasks (kernels_solve.cuh trsv_pass)
   hykkt::DBuf<int> tr_task_ptr, tr_task_sn, tr_pos;
   hykkt::DBuf<unsigned char> tr_task_big;
-  int tr_ntasks = 0;
+  int tr_ntasks = 0, tr_nbot = 0;
+  hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
   bool ruiz_rows_built = false;
@@ -315,7 +317,12 @@ void init_ctx(Ctx& c, int device) {
   c.coop_factor_blocks = occupancy_blocks(c, (const void*)dev::k_factor);
   c.coop_mf_blocks = occupancy_blocks(c, (const void*)dev::k_mf_factor);
   c.coop_trsv_blocks = occupancy_blocks(c, (const void*)dev::k_trsv);
-  c.coop_cg_blocks = occupancy_blocks(c, (const void*)dev::k_cg);
+  {
+    int minb = 2;
+    if (const char* e = std::getenv("HYKKT_CG_MINB")) minb = std::atoi(e);
+    c.cg_fn = minb >= 4 ? (const void*)dev::k_cg<4> : minb == 3 ? (const void*)dev::k_cg<3> : (const void*)dev::k_cg<2>;
+  }
+  c.coop_cg_blocks = occupancy_blocks(c, c.cg_fn);
   c.coop_ruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_ruiz), 2 * c.num_sms);
   c.coop_bfactor_blocks = occupancy_blocks(c, (const void*)dev::kb_factor, kBatchSmem);
   c.coop_btrsv_blocks = occupancy_blocks(c, (const void*)dev::kb_trsv, kBatchSmem);
@@ -332,6 +339,39 @@ void init_ctx(Ctx& c, int device) {
   CK(cudaMemsetAsync(c.barrier.p, 0, 2 * sizeof(unsigned), c.stream));
   c.status.alloc(1);
   CK(cudaMemsetAsync(c.status.p, 0, sizeof(StatusBlock), c.stream));
+}
+
+// Topological CTA task list for the solves: wide supernodes (big(sn)) are
+// whole-CTA tasks; runs of narrow supernodes between them form groups of up
+// to `group` that the CTA's warps pull from in order (reversed for the
+// backward pass).
+template <class Pred>
+void ordered_tasks(const SupernodalPlan& s, idx skip, Pred big, int group, std::vector<int>& tp,
+                   std::vector<int>& tsn, std::vector<unsigned char>& tbig) {
+  tp.assign(1, 0);
+  tsn.clear();
+  tbig.clear();
+  int open = 0;
+  auto flush = [&] {
+    if (open > 0) {
+      tp.push_back(static_cast<int>(tsn.size()));
+      tbig.push_back(0);
+      open = 0;
+    }
+  };
+  for (idx q = skip; q < s.nsup; ++q) {
+    const int sn = s.order[q];
+    if (big(sn)) {
+      flush();
+      tsn.push_back(sn);
+      tp.push_back(static_cast<int>(tsn.size()));
+      tbig.push_back(1);
+    } else {
+      tsn.push_back(sn);
+      if (++open == group) flush();
+    }
+  }
+  flush();
 }
 
 // Level-ordered CTA task list: supernodes with big(sn) are single-supernode
@@ -441,11 +481,40 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE")) wide = std::max(1ll, std::atoll(e));
     std::vector<int> tp, tsn, pos(std::max<idx>(1, s.nsup));
     std::vector<unsigned char> tbig;
-    level_tasks(s, [&](int sn) {
+    int group = 8;
+    if (const char* e = std::getenv("HYKKT_TRSV_GROUP")) group = std::max(1, std::atoi(e));
+
+    for (idx k = 0; k < s.nsup; ++k) pos[s.order[k]] = static_cast<int>(k);
+    // bottom levels: every supernode narrow enough for a thread (w <= 4,
+    // nrows <= 16) and the level wide enough to fill the GPU
+    int nbot = 0, minlev = 16384;
+    if (const char* e = std::getenv("HYKKT_TRSV_BOTTOM_MIN")) minlev = std::atoi(e);
+    std::vector<int> bptr{0}, bsn;
+    {
+      idx q = 0;
+      while (q < s.nsup) {
+        const int lev = s.sn_level[s.order[q]];
+        idx q1 = q;
+        bool ok = true;
+        while (q1 < s.nsup && s.sn_level[s.order[q1]] == lev) {
+          const int sn = s.order[q1];
+          ok = ok && s.sn_first[sn + 1] - s.sn_first[sn] <= 4 && s.sn_nrows[sn] <= 16;
+          ++q1;
+        }
+        if (!ok || q1 - q < minlev || lev != nbot) break;
+        for (idx k = q; k < q1; ++k) bsn.push_back(s.order[k]);
+        bptr.push_back(static_cast<int>(bsn.size()));
+        ++nbot;
+        q = q1;
+      }
+    }
+    c.tr_nbot = nbot;
+    c.tr_bot_ptr.upload(bptr, st);
+    c.tr_bot_sn.upload(bsn.empty() ? std::vector<int>{0} : bsn, st);
+    ordered_tasks(s, static_cast<idx>(bsn.size()), [&](int sn) {
       const long long w = s.sn_first[sn + 1] - s.sn_first[sn];
       return s.sn_nrows[sn] <= dev::kWideMaxRows && w * s.sn_nrows[sn] >= wide;
-    }, tp, tsn, tbig);
-    for (idx k = 0; k < s.nsup; ++k) pos[s.order[k]] = static_cast<int>(k);
+    }, group, tp, tsn, tbig);
     c.tr_task_ptr.upload(tp, st);
     c.tr_task_sn.upload(tsn.empty() ? std::vector<int>{0} : tsn, st);
     c.tr_task_big.upload(tbig.empty() ? std::vector<unsigned char>{0} : tbig, st);
@@ -558,6 +627,9 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.task_big = c.tr_task_big.p;
   ta.ntasks = c.tr_ntasks;
   ta.pos = c.tr_pos.p;
+  ta.nbot = c.tr_nbot;
+  ta.bot_ptr = c.tr_bot_ptr.p;
+  ta.bot_sn = c.tr_bot_sn.p;
   return ta;
 }
 
@@ -597,7 +669,7 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   a.res = &c.status.p->cg;
   a.tickets = fresh_tickets(c, cfg.cg_max_iter + 2);
   if (c.sp.nsup == 0 && c.kp.mc > 0) throw StateError("empty factor with constraints");
-  coop_launch(c, (const void*)dev::k_cg, c.coop_cg_blocks, &a);
+  coop_launch(c, c.cg_fn, c.coop_cg_blocks, &a);
   return read_status(c).cg;
 }
 

@@ -82,13 +82,18 @@ struct TrsvArgs {
   const unsigned char* task_big;
   int ntasks;
   const int* pos;             // supernode -> position in s.order (trace slots)
+  // bottom levels (w <= 4, nrows <= 16) solved level-synchronously, one
+  // thread per supernode, before / after the task passes
+  int nbot;
+  const int* bot_ptr;         // nbot + 1
+  const int* bot_sn;
 };
 
 constexpr int kWideMaxRows = 2048;  // wide (CTA) solve tasks stage nrows doubles in shared memory
 struct TrsvSmem {
   double a[kWideMaxRows];
   double t[32];
-  int task, first, count, big;
+  int task, first, count, big, next;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -488,12 +493,105 @@ __device__ void bwd_cta(const TrsvArgs& a, TrsvSmem& S, int sn) {
   }
 }
 
+// Bottom-level supernode, forward, one thread (w <= 4, nrows <= 16): the
+// same arithmetic in the same order as fwd_task's narrow branch.
+__device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
+  const SnPlan& s = a.s;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const int rp = s.rows_ptr[sn];
+  const double* P = a.panel + s.off[sn];
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    acc[q] = 0.0;
+    if (q < nr) {
+      double g = 0.0;
+      for (int e = __ldg(s.gat_ptr + rp + q), e1 = __ldg(s.gat_ptr + rp + q + 1); e < e1; ++e)
+        g += load_ready(a.u + __ldg(s.gat_idx + e), a.abort);
+      acc[q] = q < w ? rhs_at(a, f + q) - g : g;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < w) {
+      const double yk = acc[k] / __ldg(P + k * nr + k);
+      acc[k] = yk;
+#pragma unroll
+      for (int q = k + 1; q < 16; ++q) {
+        if (q < nr) {
+          const double l = __ldg(P + k * nr + q);
+          acc[q] = q < w ? fma(-l, yk, acc[q]) : fma(l, yk, acc[q]);
+        }
+      }
+    }
+  }
+  double* U = a.u + s.u_off[sn];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (q < w) stcg(a.y + f + q, acc[q]);
+    else if (q < nr) stcg(U + q - w, acc[q]);
+  }
+}
+
+__device__ __forceinline__ void bwd_thread(const TrsvArgs& a, int sn) {
+  const SnPlan& s = a.s;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const double* P = a.panel + s.off[sn];
+  const int* R = s.rows + s.rows_ptr[sn];
+  double xb[16], acc[4];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) xb[r] = (r >= w && r < nr) ? load_ready(a.x + __ldg(R + r), a.abort) : 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    acc[k] = 0.0;
+    if (k < w) {
+      double t = 0.0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r >= w && r < nr) t = fma(__ldg(P + k * nr + r), xb[r], t);
+      }
+      acc[k] = load_ready(a.y + f + k, a.abort) - t;
+    }
+  }
+#pragma unroll
+  for (int k = 3; k >= 0; --k) {
+    if (k < w) {
+      const double xk = acc[k] / __ldg(P + k * nr + k);
+      acc[k] = xk;
+#pragma unroll
+      for (int j = 0; j < k; ++j) acc[j] = fma(-__ldg(P + j * nr + k), xk, acc[j]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < w) {
+      stcg(a.x + f + k, acc[k]);
+      if (a.x_out) a.x_out[s.perm[f + k]] = acc[k];
+    }
+  }
+}
+
+// Bottom levels, forward (levels ascending) or backward (descending), one
+// grid barrier after each level.
+__device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int li = 0; li < a.nbot; ++li) {
+    const int l = fwd ? li : a.nbot - 1 - li;
+    for (int i = a.bot_ptr[l] + gt; i < a.bot_ptr[l + 1]; i += gs) {
+      if (fwd) fwd_thread(a, a.bot_sn[i]);
+      else bwd_thread(a, a.bot_sn[i]);
+    }
+    grid_sync(a.bar, a.abort);
+  }
+}
+
 // One forward + backward pass; y and x must hold kUnset on entry.  CTAs
 // take tasks in order from the ticket (forward tasks in level order, then
 // the same list reversed for the backward pass).
 __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nt = a.ntasks, ns = a.s.nsup;
+  if (a.nbot > 0) trsv_bottom(a, true);
   for (;;) {
     if (tid == 0) {
       const int t = static_cast<int>(atomicAdd(a.ticket, 1u));
@@ -503,6 +601,7 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
         S.first = a.task_ptr[ti];
         S.count = a.task_ptr[ti + 1] - a.task_ptr[ti];
         S.big = a.task_big[ti];
+        S.next = 0;
       }
     }
     __syncthreads();
@@ -516,15 +615,27 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
       if (fwd) fwd_cta(a, S, sn);
       else bwd_cta(a, S, sn);
       if (a.trace && tid == 0) a.trace[slot] = global_ns();
-    } else if (wid < S.count) {
-      const int sn = a.task_sn[S.first + wid];
-      const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
-      if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
-      if (fwd) fwd_task(a, sn, lane, slot);
-      else bwd_task(a, sn, lane, slot);
-      if (a.trace && lane == 0) a.trace[slot] = global_ns();
+    } else {
+      // narrow group (topological order): warps pull supernodes from it
+      const int first = S.first, count = S.count;
+      for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&S.next, 1);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= count) break;
+        const int sn = a.task_sn[first + (fwd ? k : count - 1 - k)];
+        const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
+        if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
+        if (fwd) fwd_task(a, sn, lane, slot);
+        else bwd_task(a, sn, lane, slot);
+        if (a.trace && lane == 0) a.trace[slot] = global_ns();
+      }
     }
     __syncthreads();
+  }
+  if (a.nbot > 0) {
+    grid_sync(a.bar, a.abort);
+    trsv_bottom(a, false);
   }
 }
 
@@ -604,7 +715,8 @@ __device__ __forceinline__ double reduce_partials(const double* partials, int sl
   return block_sum(v, scratch);
 }
 
-__global__ void __launch_bounds__(256) k_cg(CgArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
   __shared__ double scratch[33];
   __shared__ TrsvSmem S;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
