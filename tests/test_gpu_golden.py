@@ -50,8 +50,13 @@ def test_single_system_matches_golden(name):
     dev.close()
 
 
+@pytest.mark.parametrize("path", ["default", "lane"])
 @pytest.mark.parametrize("name", NAMES)
-def test_batched_matches_golden(name):
+def test_batched_matches_golden(name, path, monkeypatch):
+    """Both batched paths: system-per-CTA stream solve (default where the
+    solve vector fits shared memory) and lane-per-system (HYKKT_BATCH_PATH=lane)."""
+    if path == "lane":
+        monkeypatch.setenv("HYKKT_BATCH_PATH", "lane")
     s, cfg, perm, want = load(name)
     dev = Device(0)
     dev.analyze(s, perm)
@@ -90,3 +95,31 @@ def test_batch_of_mixed_outcomes_across_tiles():
         assert reps[k].status == r1.report.status, k
         assert abs(reps[k].cg_iterations - r1.report.cg_iterations) <= 1
     assert reps[17].status == SolveStatus.kFailedDeltaMaxExceeded
+
+
+# The single-system kernels pick per supernode between a warp and a whole CTA
+# (k_mf_factor: rows >= HYKKT_MF_BIG; k_trsv / k_cg: panel entries >=
+# HYKKT_TRSV_WIDE) and solve the bottom levels one thread per supernode
+# (levels >= HYKKT_TRSV_BOTTOM_MIN supernodes).  The golden instances are
+# small, so at the defaults most of them take the warp paths; these variants
+# force every supernode onto each alternative (pivot failures of the ladder
+# included) and must give the same answers.
+VARIANTS = {
+    "cta_everything": {"HYKKT_MF_BIG": "1", "HYKKT_TRSV_WIDE": "1", "HYKKT_TRSV_BOTTOM_MIN": "100000000"},
+    "bottom_levels": {"HYKKT_TRSV_BOTTOM_MIN": "1"},
+    "left_looking_factor": {"HYKKT_FACTOR": "ll"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("name", NAMES)
+def test_single_system_kernel_variants_match_golden(name, variant, monkeypatch):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    s, cfg, perm, want = load(name)
+    dev = Device(0)
+    dev.analyze(s, perm)  # the selection is made at analysis
+    r = dev.solve_full(s, cfg)
+    sol = r.solution.stacked() if r.solution is not None else None
+    check(r.report, sol, cfg, want)
+    dev.close()
