@@ -121,6 +121,7 @@ struct hykkt_context {
   hykkt::DBuf<unsigned char> tr_task_big;
   int tr_ntasks = 0, tr_nbot = 0;
   hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
+  hykkt::DBuf<unsigned char> tr_bot_wide;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
   bool ruiz_rows_built = false;
@@ -487,27 +488,35 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     for (idx k = 0; k < s.nsup; ++k) pos[s.order[k]] = static_cast<int>(k);
     // bottom levels: every supernode narrow enough for a thread (w <= 4,
     // nrows <= 16) and the level wide enough to fill the GPU
+    // (the w <= 8 / 32-row variant serialises each row's gathers in one
+    // thread and loses to the warp tasks at ACTIVSg10k / 70k: opt-in only)
     int nbot = 0, minlev = 16384;
     if (const char* e = std::getenv("HYKKT_TRSV_BOTTOM_MIN")) minlev = std::atoi(e);
+    const bool allow_wide = std::getenv("HYKKT_TRSV_BOTTOM_WIDE") != nullptr;
     std::vector<int> bptr{0}, bsn;
+    std::vector<unsigned char> bwide;
     {
       idx q = 0;
       while (q < s.nsup) {
         const int lev = s.sn_level[s.order[q]];
         idx q1 = q;
-        bool ok = true;
+        bool ok = true, small = true;
         while (q1 < s.nsup && s.sn_level[s.order[q1]] == lev) {
           const int sn = s.order[q1];
-          ok = ok && s.sn_first[sn + 1] - s.sn_first[sn] <= 4 && s.sn_nrows[sn] <= 16;
+          const int w = s.sn_first[sn + 1] - s.sn_first[sn], nr = s.sn_nrows[sn];
+          ok = ok && (allow_wide ? w <= 8 && nr <= 32 : w <= 4 && nr <= 16);
+          small = small && w <= 4 && nr <= 16;
           ++q1;
         }
         if (!ok || q1 - q < minlev || lev != nbot) break;
         for (idx k = q; k < q1; ++k) bsn.push_back(s.order[k]);
         bptr.push_back(static_cast<int>(bsn.size()));
+        bwide.push_back(small ? 0 : 1);
         ++nbot;
         q = q1;
       }
     }
+    c.tr_bot_wide.upload(bwide.empty() ? std::vector<unsigned char>{0} : bwide, st);
     c.tr_nbot = nbot;
     c.tr_bot_ptr.upload(bptr, st);
     c.tr_bot_sn.upload(bsn.empty() ? std::vector<int>{0} : bsn, st);
@@ -630,6 +639,7 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.nbot = c.tr_nbot;
   ta.bot_ptr = c.tr_bot_ptr.p;
   ta.bot_sn = c.tr_bot_sn.p;
+  ta.bot_wide = c.tr_bot_wide.p;
   return ta;
 }
 

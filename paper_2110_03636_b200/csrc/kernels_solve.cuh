@@ -82,11 +82,12 @@ struct TrsvArgs {
   const unsigned char* task_big;
   int ntasks;
   const int* pos;             // supernode -> position in s.order (trace slots)
-  // bottom levels (w <= 4, nrows <= 16) solved level-synchronously, one
+  // bottom levels (w <= 8, nrows <= 32) solved level-synchronously, one
   // thread per supernode, before / after the task passes
   int nbot;
   const int* bot_ptr;         // nbot + 1
   const int* bot_sn;
+  const unsigned char* bot_wide;  // per bottom level: 1 -> (w <= 8, nrows <= 32) variant
 };
 
 constexpr int kWideMaxRows = 2048;  // wide (CTA) solve tasks stage nrows doubles in shared memory
@@ -493,16 +494,17 @@ __device__ void bwd_cta(const TrsvArgs& a, TrsvSmem& S, int sn) {
   }
 }
 
-// Bottom-level supernode, forward, one thread (w <= 4, nrows <= 16): the
+// Bottom-level supernode, forward, one thread (w <= W, nrows <= NR): the
 // same arithmetic in the same order as fwd_task's narrow branch.
+template <int NR, int W>
 __device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const int rp = s.rows_ptr[sn];
   const double* P = a.panel + s.off[sn];
-  double acc[16];
+  double acc[NR];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
+  for (int q = 0; q < NR; ++q) {
     acc[q] = 0.0;
     if (q < nr) {
       double g = 0.0;
@@ -512,12 +514,12 @@ __device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < W; ++k) {
     if (k < w) {
       const double yk = acc[k] / __ldg(P + k * nr + k);
       acc[k] = yk;
 #pragma unroll
-      for (int q = k + 1; q < 16; ++q) {
+      for (int q = k + 1; q < NR; ++q) {
         if (q < nr) {
           const double l = __ldg(P + k * nr + q);
           acc[q] = q < w ? fma(-l, yk, acc[q]) : fma(l, yk, acc[q]);
@@ -527,34 +529,35 @@ __device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
   }
   double* U = a.u + s.u_off[sn];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
+  for (int q = 0; q < NR; ++q) {
     if (q < w) stcg(a.y + f + q, acc[q]);
     else if (q < nr) stcg(U + q - w, acc[q]);
   }
 }
 
+template <int NR, int W>
 __device__ __forceinline__ void bwd_thread(const TrsvArgs& a, int sn) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const double* P = a.panel + s.off[sn];
   const int* R = s.rows + s.rows_ptr[sn];
-  double xb[16], acc[4];
+  double xb[NR], acc[W];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) xb[r] = (r >= w && r < nr) ? load_ready(a.x + __ldg(R + r), a.abort) : 0.0;
+  for (int r = 0; r < NR; ++r) xb[r] = (r >= w && r < nr) ? load_ready(a.x + __ldg(R + r), a.abort) : 0.0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < W; ++k) {
     acc[k] = 0.0;
     if (k < w) {
       double t = 0.0;
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
+      for (int r = 0; r < NR; ++r) {
         if (r >= w && r < nr) t = fma(__ldg(P + k * nr + r), xb[r], t);
       }
       acc[k] = load_ready(a.y + f + k, a.abort) - t;
     }
   }
 #pragma unroll
-  for (int k = 3; k >= 0; --k) {
+  for (int k = W - 1; k >= 0; --k) {
     if (k < w) {
       const double xk = acc[k] / __ldg(P + k * nr + k);
       acc[k] = xk;
@@ -563,7 +566,7 @@ __device__ __forceinline__ void bwd_thread(const TrsvArgs& a, int sn) {
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < W; ++k) {
     if (k < w) {
       stcg(a.x + f + k, acc[k]);
       if (a.x_out) a.x_out[s.perm[f + k]] = acc[k];
@@ -577,9 +580,15 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   for (int li = 0; li < a.nbot; ++li) {
     const int l = fwd ? li : a.nbot - 1 - li;
+    const bool wide = a.bot_wide[l];
     for (int i = a.bot_ptr[l] + gt; i < a.bot_ptr[l + 1]; i += gs) {
-      if (fwd) fwd_thread(a, a.bot_sn[i]);
-      else bwd_thread(a, a.bot_sn[i]);
+      if (wide) {
+        if (fwd) fwd_thread<32, 8>(a, a.bot_sn[i]);
+        else bwd_thread<32, 8>(a, a.bot_sn[i]);
+      } else {
+        if (fwd) fwd_thread<16, 4>(a, a.bot_sn[i]);
+        else bwd_thread<16, 4>(a, a.bot_sn[i]);
+      }
     }
     grid_sync(a.bar, a.abort);
   }

@@ -60,17 +60,27 @@ for k in range(ns):
         cnt += 1
 print("producer last in %d steps; excess %.1f us; compute-only arrive sum %.1f us; compute issue-wait sum %.1f us" % (
     cnt, ex / 1e3, comp / 1e3, sum((w[k, :15, 1] - w[k, :, 0].min()).max() for k in range(ns) if w[k, 0, 0]) / 1e3))
-# phase split per L step: header ready -> phase A end (max over compute warps)
-# -> arrival (max); sums over the operator
-sa = sb = sh = 0
-print("L-step phases: k kind nseg nw nt | hdr A_end arrive (max over compute warps, ns)")
+# phase split per L step (compute warps; warps [0, ww) hold the warp tasks)
+sa = sb_w = sb_t = 0.0
+nstep = 0
+crit_w = crit_t = 0.0
+print("L-step phases: k kind nseg nw nt ww | A_end  B_end(warp-task warps)  B_end(thread warps) ns")
 for k in range(ns):
     if w[k, 0, 0] == 0 or steps[k][0] not in (0, 1):
         continue
     t0 = w[k, :, 0].min()
     rel = w[k, :15] - t0
-    h, a_, b_ = rel[:, 2].max(), rel[:, 3].max(), rel[:, 4].max()
-    sh += h; sa += a_ - h; sb += b_ - a_
-    if k % 5 == 0:
-        print(f"  {k:4d} {steps[k][0]} {steps[k][3]:4d} {steps[k][4]:3d} {steps[k][5]:4d} | {h:6d} {a_:6d} {b_:6d}")
-print("sums us: header %.1f phaseA %.1f phaseB %.1f" % (sh / 1e3, sa / 1e3, sb / 1e3))
+    ww = int(steps[k][7])
+    a_end = rel[:, 3].max()
+    bw = rel[:ww, 4].max() if ww > 0 else 0
+    bt = rel[ww:, 4].max()
+    nstep += 1
+    sa += a_end
+    if bw >= bt:
+        crit_w += bw - a_end
+    else:
+        crit_t += bt - a_end
+    if k % 4 == 0:
+        print(f"  {k:4d} {steps[k][0]} {steps[k][3]:4d} {steps[k][4]:3d} {steps[k][5]:4d} {ww:2d} | {a_end:6d} {bw:6d} {bt:6d}")
+print("L steps %d: sum A_end %.1f us; phase B critical: warp-task bound %.1f us, thread-task bound %.1f us" % (
+    nstep, sa / 1e3, crit_w / 1e3, crit_t / 1e3))
