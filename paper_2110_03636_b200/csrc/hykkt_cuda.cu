@@ -116,10 +116,9 @@ struct hykkt_context {
   hykkt::DBuf<unsigned char> mf_task_big;
   hykkt::DBuf<double> mf_ubuf;
   int mf_ntasks = 0, mf_on = 1;
-  // single-system triangular-solve CTA tasks (kernels_solve.cuh trsv_pass)
-  hykkt::DBuf<int> tr_task_ptr, tr_task_sn, tr_pos;
-  hykkt::DBuf<unsigned char> tr_task_big;
-  int tr_ntasks = 0, tr_nbot = 0;
+  // single-system triangular-solve task streams (kernels_solve.cuh trsv_pass)
+  hykkt::DBuf<int> tr_wid, tr_nar, tr_pos;
+  int tr_nwid = 0, tr_nnar = 0, tr_nbot = 0;
   hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
   hykkt::DBuf<unsigned char> tr_bot_wide;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
@@ -342,39 +341,6 @@ void init_ctx(Ctx& c, int device) {
   CK(cudaMemsetAsync(c.status.p, 0, sizeof(StatusBlock), c.stream));
 }
 
-// Topological CTA task list for the solves: wide supernodes (big(sn)) are
-// whole-CTA tasks; runs of narrow supernodes between them form groups of up
-// to `group` that the CTA's warps pull from in order (reversed for the
-// backward pass).
-template <class Pred>
-void ordered_tasks(const SupernodalPlan& s, idx skip, Pred big, int group, std::vector<int>& tp,
-                   std::vector<int>& tsn, std::vector<unsigned char>& tbig) {
-  tp.assign(1, 0);
-  tsn.clear();
-  tbig.clear();
-  int open = 0;
-  auto flush = [&] {
-    if (open > 0) {
-      tp.push_back(static_cast<int>(tsn.size()));
-      tbig.push_back(0);
-      open = 0;
-    }
-  };
-  for (idx q = skip; q < s.nsup; ++q) {
-    const int sn = s.order[q];
-    if (big(sn)) {
-      flush();
-      tsn.push_back(sn);
-      tp.push_back(static_cast<int>(tsn.size()));
-      tbig.push_back(1);
-    } else {
-      tsn.push_back(sn);
-      if (++open == group) flush();
-    }
-  }
-  flush();
-}
-
 // Level-ordered CTA task list: supernodes with big(sn) are single-supernode
 // (whole CTA) tasks, the others are grouped per level, up to one per warp.
 template <class Pred>
@@ -478,12 +444,9 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   {
     // triangular-solve task list: wide supernodes (panel >= HYKKT_TRSV_WIDE
     // entries, rows within the shared staging buffer) as CTA tasks
-    long long wide = 2048;
+    long long wide = 1024;
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE")) wide = std::max(1ll, std::atoll(e));
-    std::vector<int> tp, tsn, pos(std::max<idx>(1, s.nsup));
-    std::vector<unsigned char> tbig;
-    int group = 8;
-    if (const char* e = std::getenv("HYKKT_TRSV_GROUP")) group = std::max(1, std::atoi(e));
+    std::vector<int> pos(std::max<idx>(1, s.nsup));
 
     for (idx k = 0; k < s.nsup; ++k) pos[s.order[k]] = static_cast<int>(k);
     // bottom levels: every supernode narrow enough for a thread (w <= 4,
@@ -520,15 +483,17 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     c.tr_nbot = nbot;
     c.tr_bot_ptr.upload(bptr, st);
     c.tr_bot_sn.upload(bsn.empty() ? std::vector<int>{0} : bsn, st);
-    ordered_tasks(s, static_cast<idx>(bsn.size()), [&](int sn) {
+    std::vector<int> wid, nar;
+    for (idx q = static_cast<idx>(bsn.size()); q < s.nsup; ++q) {
+      const int sn = s.order[q];
       const long long w = s.sn_first[sn + 1] - s.sn_first[sn];
-      return s.sn_nrows[sn] <= dev::kWideMaxRows && w * s.sn_nrows[sn] >= wide;
-    }, group, tp, tsn, tbig);
-    c.tr_task_ptr.upload(tp, st);
-    c.tr_task_sn.upload(tsn.empty() ? std::vector<int>{0} : tsn, st);
-    c.tr_task_big.upload(tbig.empty() ? std::vector<unsigned char>{0} : tbig, st);
+      (s.sn_nrows[sn] <= dev::kWideMaxRows && w * s.sn_nrows[sn] >= wide ? wid : nar).push_back(sn);
+    }
+    c.tr_wid.upload(wid.empty() ? std::vector<int>{0} : wid, st);
+    c.tr_nar.upload(nar.empty() ? std::vector<int>{0} : nar, st);
+    c.tr_nwid = static_cast<int>(wid.size());
+    c.tr_nnar = static_cast<int>(nar.size());
     c.tr_pos.upload(pos, st);
-    c.tr_ntasks = static_cast<int>(tbig.size());
   }
   CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   c.epoch = 0;
@@ -631,10 +596,17 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.rhs.jval = nullptr;
   ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
   ta.trace = nullptr;
-  ta.task_ptr = c.tr_task_ptr.p;
-  ta.task_sn = c.tr_task_sn.p;
-  ta.task_big = c.tr_task_big.p;
-  ta.ntasks = c.tr_ntasks;
+  ta.wid_sn = c.tr_wid.p;
+  ta.nwid = c.tr_nwid;
+  ta.nar_sn = c.tr_nar.p;
+  ta.nnar = c.tr_nnar;
+  {
+    // CTAs reserved for the wide stream (B200 sweep at C2-C4: 48 of 296)
+    int nwc = 48;
+    if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
+    nwc = std::min({nwc, c.tr_nwid, std::max(1, c.coop_cg_blocks / 2)});
+    ta.nwc = c.tr_nwid > 0 ? nwc : 0;
+  }
   ta.pos = c.tr_pos.p;
   ta.nbot = c.tr_nbot;
   ta.bot_ptr = c.tr_bot_ptr.p;
@@ -653,7 +625,7 @@ void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, doub
   ta.rhs.b = b;
   ta.rhs.u = u;
   ta.rhs.jval = jval;
-  ta.ticket = fresh_tickets(c, 1);
+  ta.ticket = fresh_tickets(c, 2);
   coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
 }
 
@@ -677,7 +649,7 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   a.thr = cfg.small_quadratic_threshold;
   a.max_iter = cfg.cg_max_iter;
   a.res = &c.status.p->cg;
-  a.tickets = fresh_tickets(c, cfg.cg_max_iter + 2);
+  a.tickets = fresh_tickets(c, 2 * (cfg.cg_max_iter + 2));
   if (c.sp.nsup == 0 && c.kp.mc > 0) throw StateError("empty factor with constraints");
   coop_launch(c, c.cg_fn, c.coop_cg_blocks, &a);
   return read_status(c).cg;
@@ -2389,7 +2361,7 @@ int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
     dev::TrsvArgs ta = trsv_args(c);
     ta.rhs.b = c.rhat.p;
     ta.trace = tr.p;
-    ta.ticket = fresh_tickets(c, 1);
+    ta.ticket = fresh_tickets(c, 2);
     coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
     read_status(c);
     CK(cudaMemcpy(out, tr.p, 6 * ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost));

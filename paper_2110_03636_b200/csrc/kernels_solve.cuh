@@ -75,12 +75,13 @@ struct TrsvArgs {
   GridBarrier bar;
   unsigned* ticket;           // task counter of this pass (zero on entry)
   unsigned long long* trace;  // diagnostics: per-task end / start times (ns)
-  // CTA task list in level order (forward; backward runs it reversed): one
-  // wide supernode per task (whole CTA) or up to 8 narrow ones (one per warp)
-  const int* task_ptr;
-  const int* task_sn;
-  const unsigned char* task_big;
-  int ntasks;
+  // task streams (trsv_pass): wide supernodes for the first nwc CTAs,
+  // narrow ones for the warps of the others; ticket[0] / ticket[1]
+  const int* wid_sn;
+  int nwid;
+  const int* nar_sn;
+  int nnar;
+  int nwc;
   const int* pos;             // supernode -> position in s.order (trace slots)
   // bottom levels (w <= 8, nrows <= 32) solved level-synchronously, one
   // thread per supernode, before / after the task passes
@@ -594,53 +595,46 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
   }
 }
 
-// One forward + backward pass; y and x must hold kUnset on entry.  CTAs
-// take tasks in order from the ticket (forward tasks in level order, then
-// the same list reversed for the backward pass).
+// One forward + backward pass; y and x must hold kUnset on entry.
+// Two task streams, each in topological order (forward list, then the same
+// list reversed for the backward pass):
+//   wide supernodes -> CTA tasks on the first `nwc` CTAs (ticket[0]);
+//   narrow ones     -> warp tasks on every warp of the other CTAs (ticket[1]).
+// Both streams follow one global topological order and each is taken in
+// order, so the smallest unfinished task always has its dependencies held by
+// running CTAs / warps: no deadlock.
 __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nt = a.ntasks, ns = a.s.nsup;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int ns = a.s.nsup;
   if (a.nbot > 0) trsv_bottom(a, true);
-  for (;;) {
-    if (tid == 0) {
-      const int t = static_cast<int>(atomicAdd(a.ticket, 1u));
-      S.task = t;
-      if (t < 2 * nt) {
-        const int ti = t < nt ? t : 2 * nt - 1 - t;
-        S.first = a.task_ptr[ti];
-        S.count = a.task_ptr[ti + 1] - a.task_ptr[ti];
-        S.big = a.task_big[ti];
-        S.next = 0;
-      }
-    }
-    __syncthreads();
-    const int t = S.task;
-    if (t >= 2 * nt) break;
-    const bool fwd = t < nt;
-    if (S.big) {
-      const int sn = a.task_sn[S.first];
+  if (static_cast<int>(blockIdx.x) < a.nwc) {
+    const int nt = a.nwid;
+    for (;;) {
+      if (tid == 0) S.task = static_cast<int>(atomicAdd(a.ticket, 1u));
+      __syncthreads();
+      const int t = S.task;
+      __syncthreads();
+      if (t >= 2 * nt) break;
+      const bool fwd = t < nt;
+      const int sn = a.wid_sn[fwd ? t : 2 * nt - 1 - t];
       const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
       if (a.trace && tid == 0) a.trace[2 * ns + slot] = global_ns();
       if (fwd) fwd_cta(a, S, sn);
       else bwd_cta(a, S, sn);
       if (a.trace && tid == 0) a.trace[slot] = global_ns();
-    } else {
-      // narrow group (topological order): warps pull supernodes from it
-      const int first = S.first, count = S.count;
-      for (;;) {
-        int k = 0;
-        if (lane == 0) k = atomicAdd(&S.next, 1);
-        k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= count) break;
-        const int sn = a.task_sn[first + (fwd ? k : count - 1 - k)];
-        const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
-        if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
-        if (fwd) fwd_task(a, sn, lane, slot);
-        else bwd_task(a, sn, lane, slot);
-        if (a.trace && lane == 0) a.trace[slot] = global_ns();
-      }
+      __syncthreads();
     }
-    __syncthreads();
+  } else {
+    const int nt = a.nnar;
+    for (long long t = grab_task(a.ticket + 1, lane); t < 2 * nt; t = grab_task(a.ticket + 1, lane)) {
+      const bool fwd = t < nt;
+      const int sn = a.nar_sn[fwd ? t : 2 * nt - 1 - t];
+      const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
+      if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
+      if (fwd) fwd_task(a, sn, lane, slot);
+      else bwd_task(a, sn, lane, slot);
+      if (a.trace && lane == 0) a.trace[slot] = global_ns();
+    }
   }
   if (a.nbot > 0) {
     grid_sync(a.bar, a.abort);
@@ -754,7 +748,7 @@ __global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
   double r_norm = rhs_norm;
   TrsvArgs tr = a.tr;
   for (long long it = 1; it <= a.max_iter; ++it) {
-    tr.ticket = a.tickets + it;
+    tr.ticket = a.tickets + 2 * it;
     trsv_pass(tr, S);
     grid_sync(bar, abort);
     double pq = 0.0, pp = 0.0;
