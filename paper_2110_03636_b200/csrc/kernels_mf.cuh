@@ -296,7 +296,7 @@ __device__ void mf_cta_task(const MfArgs& a, MfSmem& S, int sn, double floor_v) 
   }
 }
 
-__global__ void __launch_bounds__(kMfThreads) k_mf_factor(MfArgs a) {
+__global__ void __launch_bounds__(kMfThreads, 2) k_mf_factor(MfArgs a) {
   __shared__ MfSmem S;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double floor_v = fmax(a.maxdiag ? a.floor_rel * *a.maxdiag : a.floor_abs, 0.0);
