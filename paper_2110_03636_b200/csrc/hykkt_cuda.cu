@@ -606,6 +606,8 @@ dev::TrsvArgs trsv_args(Ctx& c) {
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
     nwc = std::min({nwc, c.tr_nwid, std::max(1, c.coop_cg_blocks / 2)});
     ta.nwc = c.tr_nwid > 0 ? nwc : 0;
+    ta.pre_wait = 10;  // narrow tasks poll their own values (B200 sweep; the general ones need the pre-wait)
+    if (const char* e = std::getenv("HYKKT_TRSV_PREWAIT")) ta.pre_wait = std::atoi(e);
   }
   ta.pos = c.tr_pos.p;
   ta.nbot = c.tr_nbot;

@@ -82,6 +82,10 @@ struct TrsvArgs {
   const int* nar_sn;
   int nnar;
   int nwc;
+  // narrow tasks: poll one flag value before loading (bit 0 fwd narrow,
+  // 1 fwd general, 2 bwd narrow, 3 bwd general); otherwise every value is
+  // polled where it is loaded
+  int pre_wait;
   const int* pos;             // supernode -> position in s.order (trace slots)
   // bottom levels (w <= 8, nrows <= 32) solved level-synchronously, one
   // thread per supernode, before / after the task passes
@@ -183,7 +187,7 @@ __device__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) lrow[k] = (row && k < w) ? __ldg(P + k * nr + lane) : 0.0;
     const double bi = own ? rhs_at(a, f + lane) : 0.0;
-    wait_children(a, sn, lane);
+    if (a.pre_wait & 1) wait_children(a, sn, lane);
     double xv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) xv[k] = gi[k] >= 0 ? ldcg(a.u + gi[k]) : 0.0;
@@ -213,7 +217,7 @@ __device__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
   // b - (children's contributions) and for rows below, the running update.
   double* A = a.acc_buf + rp;
   for (int q = lane; q < nr; q += 32) A[q] = q < w ? rhs_at(a, f + q) : 0.0;
-  wait_children(a, sn, lane);
+  if (a.pre_wait & 2) wait_children(a, sn, lane);
   // Extend-add the children's update vectors (child-side relative indices:
   // coalesced, four loads in flight per lane).
   for (int c = s.child_ptr[sn]; c < s.child_ptr[sn + 1]; ++c) {
@@ -295,7 +299,7 @@ __device__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
     for (int k = 0; k < 4; ++k) lv[k] = (lane < below && k < w) ? __ldg(P + k * nr + w + lane) : 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) ld[k] = (lane < w && k < w) ? __ldg(P + lane * nr + k) : 0.0;  // L(k, lane)
-    wait_parent(a, sn, lane);
+    if (a.pre_wait & 4) wait_parent(a, sn, lane);
     double acc = lane < w ? load_ready(a.y + f + lane, a.abort) : 0.0;
     const double xr = lane < below ? load_ready(a.x + gr, a.abort) : 0.0;
     if (a.trace) { __syncwarp(); if (lane == 0) a.trace[4 * a.s.nsup + tslot] = global_ns(); }
@@ -326,7 +330,7 @@ __device__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
     double d[32];  // column cb+lane of the chunk's diagonal block: L(cb+k, cb+lane)
 #pragma unroll
     for (int k = 0; k < 32; ++k) d[k] = (k < cw && lane < cw) ? __ldg(P + (cb + lane) * nr + cb + k) : 0.0;
-    if (ci == nchunks - 1) wait_parent(a, sn, lane);
+    if (ci == nchunks - 1 && (a.pre_wait & 8)) wait_parent(a, sn, lane);
     double acc = lane < cw ? load_ready(a.y + f + cb + lane, a.abort) : 0.0;
     const int rb0 = cb + cw;  // rows below this chunk (own later chunks + ancestors)
     double t = 0.0;           // lane = column: sum_r L(r, cb+lane) x_r
