@@ -337,7 +337,7 @@ __device__ __forceinline__ void ks_bwd_thread(const KsRing& R, double* v, const 
   }
 }
 
-// Warp task (width > HYKKT_THREAD_TASK_W): lanes = rows (forward) /
+// Warp task (width > thread_task_w(), sysplan.cpp): lanes = rows (forward) /
 // columns (backward) of a 32-block, shuffle triangular solve.
 __device__ __forceinline__ void ks_warp_task(const KsRing& R, double* v, const double* part, int voff, int ioff,
                                              int f, int w, bool bwd, int lane) {

@@ -25,6 +25,11 @@ int inline_max() {
   static const int v = std::getenv("HYKKT_KS_INLINE") ? std::atoi(std::getenv("HYKKT_KS_INLINE")) : 8;
   return v;
 }
+// widest supernode a single thread solves (wider ones are warp tasks)
+int thread_task_w() {
+  static const int v = std::getenv("HYKKT_KS_THREAD_W") ? std::atoi(std::getenv("HYKKT_KS_THREAD_W")) : 3;
+  return v;
+}
 constexpr int kMinSeg = 8;
 
 struct Seg {
@@ -116,7 +121,7 @@ struct Builder {
     const long long off = sp.sn_off[s];
     t.f = f;
     t.w = w;
-    t.warp = w > HYKKT_THREAD_TASK_W;
+    t.warp = w > thread_task_w();
     long long g = 0;
     if (!bwd) {
       for (int r = 0; r < w; ++r) g += row_gather(f + r);
@@ -236,8 +241,10 @@ struct Builder {
     // warps [0, ww) take the warp tasks; thread tasks are dealt over the
     // remaining NT - 32 ww threads (sysplan_format.h header word 7)
     const int nwarps = P.nthreads / 32;
+    static const int wwk = std::getenv("HYKKT_KS_WW8") ? std::atoi(std::getenv("HYKKT_KS_WW8")) : 5;  // eighths of the warps (B200 sweep)
     const int ww = warp.empty() ? 0 : thr.empty() ? std::min<int>(static_cast<int>(warp.size()), nwarps)
-                                                  : std::min<int>(static_cast<int>(warp.size()), std::max(1, nwarps / 2));
+                                                  : std::min<int>(static_cast<int>(warp.size()),
+                                                                  std::max(1, std::min(nwarps - 1, nwarps * wwk / 8)));
     // deal thread tasks: thread t takes positions t, t + NT, ...; snake order
     // over the full rounds balances every thread's total cost
     {
@@ -512,7 +519,7 @@ double sys_plan_selfcheck(const SupernodalPlan& sp, const KktPlan& kp, const Sys
         for (int t = 0; t < nw + nt; ++t) {
           const int d = HYKKT_SP_HDR + HYKKT_SP_SEG_INTS * nseg + HYKKT_SP_TASK_INTS * t;
           const int voff = I(d), ioff = I(d + 1), f = I(d + 2), w = I(d + 3) & 0xffff, mode = I(d + 3) >> 16;
-          if ((t < nw) != (w > HYKKT_THREAD_TASK_W)) throw InvalidArgument("sys plan selfcheck: task kind mismatch");
+          if ((t < nw) != (w > thread_task_w())) throw InvalidArgument("sys plan selfcheck: task kind mismatch");
           const bool inl = mode == HYKKT_TASK_INLINE;
           if (!bwd) {
             long long e = voff + w * (w + 1) / 2;

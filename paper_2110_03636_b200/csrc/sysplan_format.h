@@ -44,8 +44,9 @@
 #define HYKKT_TASK_INLINE 1
 #define HYKKT_TASK_SEGMENTED 2
 
-// widest supernode a single thread solves; wider ones are warp tasks
-#define HYKKT_THREAD_TASK_W 8
+// The widest supernode a single thread solves is a host-side choice
+// (sysplan.cpp thread_task_w(), default 3 from the B200 sweep): the device
+// reads the task kind from the step header, not from the width.
 
 // Value stream source encoding (int32):
 //   s >= 0   panel slot (s >> 1); (s & 1) = store the reciprocal
