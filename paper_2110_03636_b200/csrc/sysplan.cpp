@@ -30,7 +30,11 @@ int thread_task_w() {
   static const int v = std::getenv("HYKKT_KS_THREAD_W") ? std::atoi(std::getenv("HYKKT_KS_THREAD_W")) : 3;
   return v;
 }
-constexpr int kMinSeg = 8;
+// shortest segment (partial dot product) of a long gather
+int min_seg() {
+  static const int v = std::getenv("HYKKT_KS_MINSEG") ? std::max(1, std::atoi(std::getenv("HYKKT_KS_MINSEG"))) : 8;
+  return v;
+}
 
 struct Seg {
   std::vector<int> vsrc;  // value sources
@@ -222,7 +226,7 @@ struct Builder {
     std::vector<Task> g;
     g.reserve(sns.size());
     for (int s : sns) g.push_back(make_task(s, bwd));
-    int sl = kMinSeg;
+    int sl = min_seg();
     while (seg_count(sns, g, bwd, sl) > P.pmax) {
       sl *= 2;
       if (sl > capv / 4) throw InvalidArgument("sys plan: too many segments for the partials array");
