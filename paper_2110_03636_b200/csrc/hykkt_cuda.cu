@@ -131,7 +131,7 @@ struct hykkt_context {
 
   // device supernodal plan
   hykkt::DBuf<int> order, first, nrows, off, rows_ptr, rows, parent, child_ptr, child;
-  hykkt::DBuf<int> upd_ptr, upd_d, upd_off, upd_cnt, lrow_ptr, lrow_col, lrow_pos, lrow_row;
+  hykkt::DBuf<int> upd_ptr, upd_d, upd_off, upd_cnt, lrow_ptr, lrow_col, lrow_pos, lrow_row, upd_pbase, upd_pos;
   hykkt::DBuf<double> lrow_val, xsol, ubuf, accbuf;
   hykkt::DBuf<int> u_off, ext_ptr, ext_map, gat_ptr, gat_idx, relind;
   hykkt::DBuf<int> perm, iperm, src_to_panel, src_row, src_col;
@@ -227,6 +227,8 @@ struct hykkt_context {
     s.gat_idx = gat_idx.p;
     s.relind = relind.p;
     s.u_size = sp.u_off.empty() ? 0 : sp.u_off.back();
+    s.upd_pbase = upd_pbase.p;
+    s.upd_pos = upd_pos.p;
     return s;
   }
 
@@ -388,6 +390,28 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   c.upd_d.upload(s.upd_d, st);
   c.upd_off.upload(s.upd_off, st);
   c.upd_cnt.upload(s.upd_cnt, st);
+  {
+    // positions of every descendant row of every left-looking update in the
+    // target's row structure (replaces a per-entry binary search on device)
+    std::vector<int> pbase(s.upd_d.size() + 1, 0), pos;
+    for (idx t = 0; t < s.nsup; ++t) {
+      const int f = s.sn_first[t], w = s.sn_first[t + 1] - f;
+      const int* R = s.sn_rows.data() + s.sn_rows_ptr[t];
+      const int* Re = s.sn_rows.data() + s.sn_rows_ptr[t + 1];
+      for (int u = s.upd_ptr[t]; u < s.upd_ptr[t + 1]; ++u) {
+        const int d = s.upd_d[u], o = s.upd_off[u], cnt = s.upd_cnt[u];
+        const int* Rd = s.sn_rows.data() + s.sn_rows_ptr[d];
+        const int m = s.sn_nrows[d] - o;
+        for (int ii = 0; ii < m; ++ii) {
+          const int r = Rd[o + ii];
+          pos.push_back(ii < cnt ? r - f : static_cast<int>(std::lower_bound(R + w, Re, r) - R));
+        }
+        pbase[u + 1] = static_cast<int>(pos.size());
+      }
+    }
+    c.upd_pbase.upload(pbase, st);
+    c.upd_pos.upload(pos.empty() ? std::vector<int>{0} : pos, st);
+  }
   c.lrow_ptr.upload(s.lrow_ptr, st);
   c.lrow_col.upload(s.lrow_col, st);
   c.lrow_pos.upload(s.lrow_pos, st);

@@ -347,6 +347,7 @@ struct BFactorArgs {
 // stores to possibly-aliasing global addresses, so without the explicit
 // blocking every step of a lane's sequential loop would pay an L2 round trip.
 constexpr int kIlp = 8;
+constexpr int kUb = 4;  // descendant rows held in registers per left-looking update block
 
 __device__ void bfactor_task(const BFactorArgs& a, int sn, int tile, int lane) {
   const SnPlan& s = a.s;
@@ -369,36 +370,46 @@ __device__ void bfactor_task(const BFactorArgs& a, int sn, int tile, int lane) {
       const double* Pd = a.panel + (long long)s.off[d] * Bp + b;
       const int* Rd = s.rows + s.rows_ptr[d];
       const int m = nrd - o;
-      for (int jj = 0; jj < cnt; ++jj) {
-        const int cc = __ldg(Rd + o + jj) - f;
-        for (int k0 = 0; k0 < wd; k0 += 4) {
-          const int kn = min(4, wd - k0);
-          double lj[4];
+      const int* upos = s.upd_pos + s.upd_pbase[u];
+      // k-blocks of 4 descendant columns; for each block of kUb descendant
+      // rows the row values stay in registers while every target column jj
+      // (<= the block's last row) is updated: each target entry receives its
+      // k-block dots in ascending k0, as a plain left-looking sweep would.
+      for (int k0 = 0; k0 < wd; k0 += 4) {
+        const int kn = min(4, wd - k0);
+        for (int i0 = 0; i0 < m; i0 += kUb) {
+          double li[kUb][4];
+          int pos[kUb];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) lj[k] = k < kn ? ldcg(Pd + (long long)((k0 + k) * nrd + o + jj) * Bp) : 0.0;
-          for (int i0 = jj; i0 < m; i0 += kIlp) {
-            double dot[kIlp];
-            int pos[kIlp];
+          for (int t = 0; t < kUb; ++t) {
+            const int ii = i0 + t;
+            pos[t] = ii < m ? __ldg(upos + ii) : -1;
 #pragma unroll
-            for (int t = 0; t < kIlp; ++t) {
-              const int ii = i0 + t;
-              dot[t] = 0.0;
-              pos[t] = -1;
-              if (ii < m) {
+            for (int k = 0; k < 4; ++k)
+              li[t][k] = (ii < m && k < kn) ? ldcg(Pd + (long long)((k0 + k) * nrd + o + ii) * Bp) : 0.0;
+          }
+          const int jend = min(cnt, i0 + kUb);
+          for (int jj = 0; jj < jend; ++jj) {
+            const int cc = __ldg(Rd + o + jj) - f;
+            double lj[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) lj[k] = k < kn ? ldcg(Pd + (long long)((k0 + k) * nrd + o + jj) * Bp) : 0.0;
+            double cur[kUb];
+#pragma unroll
+            for (int t = 0; t < kUb; ++t) {
+              const bool ok = pos[t] >= 0 && i0 + t >= jj;
+              cur[t] = ok ? P[(long long)(cc * nr + pos[t]) * Bp] : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < kUb; ++t) {
+              if (pos[t] >= 0 && i0 + t >= jj) {
+                double dot = 0.0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                  if (k < kn) dot[t] = fma(ldcg(Pd + (long long)((k0 + k) * nrd + o + ii) * Bp), lj[k], dot[t]);
+                  if (k < kn) dot = fma(li[t][k], lj[k], dot);
                 }
-                const int r = __ldg(Rd + o + ii);
-                pos[t] = (ii < cnt) ? (r - f) : find_row(R, w, nr, r);
+                P[(long long)(cc * nr + pos[t]) * Bp] = cur[t] - dot;
               }
-            }
-            double cur[kIlp];
-#pragma unroll
-            for (int t = 0; t < kIlp; ++t) cur[t] = pos[t] >= 0 ? P[(long long)(cc * nr + pos[t]) * Bp] : 0.0;
-#pragma unroll
-            for (int t = 0; t < kIlp; ++t) {
-              if (pos[t] >= 0) P[(long long)(cc * nr + pos[t]) * Bp] = cur[t] - dot[t];
             }
           }
         }

@@ -50,6 +50,10 @@ struct SnPlan {
   const int* gat_idx;
   const int* relind;
   int u_size;
+  // left-looking update u, descendant row ii (from upd_off): position of that
+  // row in the target's row structure, at upd_pos[upd_pbase[u] + ii]
+  const int* upd_pbase;
+  const int* upd_pos;
 };
 
 struct FactorArgs {
