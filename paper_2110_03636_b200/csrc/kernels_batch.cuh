@@ -520,21 +520,8 @@ __device__ void wfactor_task(const BFactorArgs& a, int sn, int b, double* sm) {
             const int k = e / m, ii = e - k * m;
             V[e] = a.panel[pan_addr(s, a.mode, d, k * nrd + o + ii, Bp, b)];
           }
-          for (int ii = tid; ii < m; ii += blockDim.x) {
-            const int r = __ldg(Rd + o + ii);
-            int pos;
-            if (ii < cnt) {
-              pos = r - f;
-            } else {
-              int lo = w, hi = nr;
-              while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (RS[mid] <= r) lo = mid; else hi = mid;
-              }
-              pos = lo;
-            }
-            POS[ii] = pos;
-          }
+          const int* upos = s.upd_pos + s.upd_pbase[u];
+          for (int ii = tid; ii < m; ii += blockDim.x) POS[ii] = __ldg(upos + ii);
           o2 += m * wd + (m + 1) / 2 + 1;
         }
       }
@@ -561,17 +548,7 @@ __device__ void wfactor_task(const BFactorArgs& a, int sn, int b, double* sm) {
                 dot = fma(a.panel[pan_addr(s, a.mode, d, k * nrd + o + ii, Bp, b)],
                           a.panel[pan_addr(s, a.mode, d, k * nrd + o + jj, Bp, b)], dot);
               }
-              const int r = __ldg(Rd + o + ii);
-              if (ii < cnt) {
-                pos = r - f;
-              } else {
-                int lo = w, hi = nr;
-                while (hi - lo > 1) {
-                  const int mid = (lo + hi) >> 1;
-                  if (RS[mid] <= r) lo = mid; else hi = mid;
-                }
-                pos = lo;
-              }
+              pos = __ldg(s.upd_pos + s.upd_pbase[u] + ii);
             }
             PS[cc * nr + pos] -= dot;
           }
