@@ -55,7 +55,7 @@ struct MfArgs {
 constexpr int kMfThreads = 256;
 constexpr int kMfNb = 32;   // column block of the wide-panel factor
 constexpr int kMfBM = 64;   // GEMM tile rows
-constexpr int kMfBK = 16;   // GEMM k-tile
+constexpr int kMfBK = 32;   // GEMM k-tile
 
 struct MfSmem {
   double a[kMfBK][kMfBM + 1];
@@ -71,6 +71,7 @@ template <int BN>
 __device__ void mf_gemm_nt_sub(MfSmem& S, double* C, int ldc, const double* A, int lda, const double* B, int ldb,
                                int M, int N, int K, int diag) {
   constexpr int TM = kMfBM / 16, TN = BN / 16;
+  constexpr int LA = kMfBK * kMfBM / kMfThreads, LB = kMfBK * BN / kMfThreads;  // loads per thread
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int tiles_m = (M + kMfBM - 1) / kMfBM, tiles_n = (N + BN - 1) / BN;
   for (int tile = 0; tile < tiles_m * tiles_n; ++tile) {
@@ -82,20 +83,37 @@ __device__ void mf_gemm_nt_sub(MfSmem& S, double* C, int ldc, const double* A, i
     for (int p = 0; p < TM; ++p)
 #pragma unroll
       for (int q = 0; q < TN; ++q) acc[p][q] = 0.0;
+    // k-tiles are prefetched into registers one tile ahead, so their L2
+    // latency overlaps the previous tile's FMAs
+    double ra[LA], rb[LB];
+    auto load = [&](int k0) {
+#pragma unroll
+      for (int l = 0; l < LA; ++l) {
+        const int e = tid + l * kMfThreads, i = e % kMfBM, k = e / kMfBM;
+        ra[l] = (i0 + i < M && k0 + k < K) ? ldcg(A + (i0 + i) + static_cast<long long>(k0 + k) * lda) : 0.0;
+      }
+#pragma unroll
+      for (int l = 0; l < LB; ++l) {
+        const int e = tid + l * kMfThreads, j = e % BN, k = e / BN;
+        rb[l] = (j0 + j < N && k0 + k < K) ? ldcg(B + (j0 + j) + static_cast<long long>(k0 + k) * ldb) : 0.0;
+      }
+    };
+    load(0);
     for (int k0 = 0; k0 < K; k0 += kMfBK) {
       __syncthreads();
-      for (int e = tid; e < kMfBK * kMfBM; e += kMfThreads) {
-        const int i = e % kMfBM, k = e / kMfBM;
-        const bool ok = i0 + i < M && k0 + k < K;
-        S.a[k][i] = ok ? ldcg(A + (i0 + i) + static_cast<long long>(k0 + k) * lda) : 0.0;
+#pragma unroll
+      for (int l = 0; l < LA; ++l) {
+        const int e = tid + l * kMfThreads;
+        S.a[e / kMfBM][e % kMfBM] = ra[l];
       }
-      for (int e = tid; e < kMfBK * BN; e += kMfThreads) {
-        const int j = e % BN, k = e / BN;
-        const bool ok = j0 + j < N && k0 + k < K;
-        S.b[k][j] = ok ? ldcg(B + (j0 + j) + static_cast<long long>(k0 + k) * ldb) : 0.0;
+#pragma unroll
+      for (int l = 0; l < LB; ++l) {
+        const int e = tid + l * kMfThreads;
+        S.b[e / BN][e % BN] = rb[l];
       }
       __syncthreads();
-#pragma unroll 4
+      if (k0 + kMfBK < K) load(k0 + kMfBK);
+#pragma unroll 8
       for (int k = 0; k < kMfBK; ++k) {
         double av[TM], bv[TN];
 #pragma unroll
