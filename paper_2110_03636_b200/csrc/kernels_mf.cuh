@@ -149,19 +149,33 @@ __device__ __forceinline__ void mf_extend_add(const MfArgs& a, int s, int c, dou
   const int mcc = p.nrows[c] - (p.first[c + 1] - p.first[c]);
   const double* Uc = a.ubuf + a.uoff[c];
   const int* ri = p.relind + p.u_off[c];
-  // lower triangle of Uc, column by column
-  for (int t2 = 0; t2 < mcc; ++t2) {
-    const int r2 = __ldg(ri + t2);
-    for (int t1 = t2 + t; t1 < mcc; t1 += nt) {
-      const int r1 = __ldg(ri + t1);
-      const double v = ldcg(Uc + t1 + static_cast<long long>(t2) * mcc);
-      if (r2 < w) {
-        double* q = P + r1 + static_cast<long long>(r2) * nr;
-        *q = ldcg(q) + v;
-      } else {
-        double* q = U + (r1 - w) + static_cast<long long>(r2 - w) * m;
-        *q = ldcg(q) + v;
+  // lower triangle of Uc over the flattened square (e = t1 + t2 mcc), four
+  // entries per thread in flight: the map is injective within one child, so
+  // the four read-modify-writes never alias
+  const long long tot = static_cast<long long>(mcc) * mcc;
+  for (long long e0 = t; e0 < tot; e0 += 4ll * nt) {
+    double v[4];
+    double* q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long long e = e0 + static_cast<long long>(j) * nt;
+      q[j] = nullptr;
+      v[j] = 0.0;
+      if (e < tot) {
+        const int t2 = static_cast<int>(e / mcc), t1 = static_cast<int>(e - static_cast<long long>(t2) * mcc);
+        if (t1 >= t2) {
+          const int r1 = __ldg(ri + t1), r2 = __ldg(ri + t2);
+          v[j] = ldcg(Uc + e);
+          q[j] = r2 < w ? P + r1 + static_cast<long long>(r2) * nr : U + (r1 - w) + static_cast<long long>(r2 - w) * m;
+        }
       }
+    }
+    double cur[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cur[j] = q[j] ? ldcg(q[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (q[j]) *q[j] = cur[j] + v[j];
     }
   }
   (void)s;
