@@ -1205,12 +1205,16 @@ void build_batch_jobs(Ctx& c, int T) {
 
 // ---- system-per-CTA solve (kernels_sys.cuh) ---------------------------------
 constexpr int kKsThreads = 512;
-constexpr int kKsChunkLg = 10;  // 1024-entry TMA chunks (8 KB values, 4 KB indices)
+// ring chunk: 2^lg entries (lg = 10: 8 KB of values, 4 KB of indices)
+int ks_chunk_lg() {
+  static const int v = std::getenv("HYKKT_KS_CHUNK_LG") ? std::max(8, std::min(12, std::atoi(std::getenv("HYKKT_KS_CHUNK_LG")))) : 10;
+  return v;
+}
 constexpr int kKsPmax = 1024;
 
 std::size_t ks_smem_bytes(idx n, int nv, int ni) {
   const std::size_t vbytes = (static_cast<std::size_t>(n) * 8 + 127) & ~static_cast<std::size_t>(127);
-  return (static_cast<std::size_t>(nv) * 8 + static_cast<std::size_t>(ni) * 4) * (std::size_t{1} << kKsChunkLg) +
+  return (static_cast<std::size_t>(nv) * 8 + static_cast<std::size_t>(ni) * 4) * (std::size_t{1} << ks_chunk_lg()) +
          8 * static_cast<std::size_t>(nv + ni) + 8 * 66 + 64 + 8 * dev::kPrN + 8 * kKsPmax + vbytes;
 }
 
@@ -1279,7 +1283,7 @@ bool ks_prepare(Ctx& c) {
   }
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
-  int nch = 16;
+  int nch = 16 << std::max(0, 10 - ks_chunk_lg());
   while (nch >= 4 && ks_smem_bytes(sp.n, nch, nch) > static_cast<std::size_t>(optin)) nch /= 2;
   if (nch < 4) {
     ks.why = "solve vector does not fit shared memory";
@@ -1290,7 +1294,7 @@ bool ks_prepare(Ctx& c) {
     // one-step lookahead (measured: 62 -> 54 ms per 256-system CG launch)
     int step_chunks = nch - 2;
     if (const char* e = std::getenv("HYKKT_KS_STEP_CHUNKS")) step_chunks = std::atoi(e);
-    ks.plan = build_sys_plan(sp, c.kp, kKsChunkLg, nch, kKsChunkLg, nch, kKsPmax, kKsThreads - 32, step_chunks);
+    ks.plan = build_sys_plan(sp, c.kp, ks_chunk_lg(), nch, ks_chunk_lg(), nch, kKsPmax, kKsThreads - 32, step_chunks);
   } catch (const InvalidArgument& e) {
     ks.why = e.what();
     return false;
@@ -2112,7 +2116,7 @@ int hykkt_debug_sysplan_check(int64_t n_x, int64_t m_c, int64_t m_d, const int64
     std::vector<idx> pv;
     if (perm) pv.assign(perm, perm + n_x);
     const SupernodalPlan sp = build_supernodal_plan(kp.hg, std::move(pv));
-    const SysPlan P = build_sys_plan(sp, kp, kKsChunkLg, nchunk, kKsChunkLg, nchunk, kKsPmax, kKsThreads - 32);
+    const SysPlan P = build_sys_plan(sp, kp, ks_chunk_lg(), nchunk, ks_chunk_lg(), nchunk, kKsPmax, kKsThreads - 32);
     out[0] = sys_plan_selfcheck(sp, kp, P, 12345u);
     out[1] = static_cast<double>(P.src.size());
     out[2] = static_cast<double>(P.idx.size());
