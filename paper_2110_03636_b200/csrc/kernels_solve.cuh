@@ -96,6 +96,7 @@ struct TrsvArgs {
 };
 
 constexpr int kWideMaxRows = 2048;  // wide (CTA) solve tasks stage nrows doubles in shared memory
+constexpr int kWarpRows = kWideMaxRows / 8;  // narrow-task CTAs: each warp's slice of the same buffer
 struct TrsvSmem {
   double a[kWideMaxRows];
   double t[32];
@@ -166,7 +167,7 @@ __device__ __forceinline__ void wait_children(const TrsvArgs& a, int sn, int lan
 // y = L_ss^-1 (b - acc), rows below: u_s = acc + L_below y, handed to the
 // parent.  Every static load (gather indices, L, right-hand side) is issued
 // before the first wait, so a tree level costs about one L2 round trip.
-__device__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
+__device__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot, double* sA = nullptr) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const int rp = s.rows_ptr[sn];
@@ -215,8 +216,10 @@ __device__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
   }
   // General supernode: A[q] (per-supernode scratch) holds, for own rows,
   // b - (children's contributions) and for rows below, the running update.
-  double* A = a.acc_buf + rp;
+  // (the warp's slice of shared memory when the caller has one and the rows fit)
+  double* A = (sA && nr <= kWarpRows) ? sA : a.acc_buf + rp;
   for (int q = lane; q < nr; q += 32) A[q] = q < w ? rhs_at(a, f + q) : 0.0;
+  __syncwarp();
   if (a.pre_wait & 2) wait_children(a, sn, lane);
   // Extend-add the children's update vectors (child-side relative indices:
   // coalesced, four loads in flight per lane).
@@ -635,7 +638,7 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
       const int sn = a.nar_sn[fwd ? t : 2 * nt - 1 - t];
       const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
       if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
-      if (fwd) fwd_task(a, sn, lane, slot);
+      if (fwd) fwd_task(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
       else bwd_task(a, sn, lane, slot);
       if (a.trace && lane == 0) a.trace[slot] = global_ns();
     }
