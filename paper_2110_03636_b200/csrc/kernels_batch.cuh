@@ -553,6 +553,8 @@ __device__ void wfactor_task(const BFactorArgs& a, int sn, int b, double* sm) {
             PS[cc * nr + pos] -= dot;
           }
         }
+        // the next update may hit the same entries from other lanes
+        __syncwarp();
         if (staged) o2 += m * wd + (m + 1) / 2 + 1;
       }
       __syncthreads();

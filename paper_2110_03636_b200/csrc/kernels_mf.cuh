@@ -280,7 +280,7 @@ __device__ void mf_cta_task(const MfArgs& a, MfSmem& S, int sn, double floor_v) 
           __syncwarp();
           if (lane > k) S.d[k][lane] /= dk;
           __syncwarp();
-          if (lane == 0) S.d[k][k] = dk;
+          if (lane == k) S.d[k][k] = dk;  // the row's owner: no cross-lane hazard
           const double lrk = S.d[k][lane];
           for (int c = k + 1; c < jb; ++c) {
             if (lane >= c) S.d[c][lane] = fma(-lrk, S.d[k][c], S.d[c][lane]);
