@@ -447,7 +447,7 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     // multifrontal factor: update-matrix offsets and the level-ordered task
     // list (one wide supernode per CTA task, up to 8 narrow ones of a level
     // per warp-group task)
-    int big_rows = 64;
+    int big_rows = 24;  // B200 sweep at C2-C4 (was 64: C2 factor 1.24 -> 0.77 ms)
     if (const char* e = std::getenv("HYKKT_MF_BIG")) big_rows = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("HYKKT_FACTOR")) c.mf_on = std::string(e) != "ll";
     std::vector<long long> uo(s.nsup + 1, 0);
