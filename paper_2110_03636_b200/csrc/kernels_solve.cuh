@@ -100,7 +100,7 @@ constexpr int kWarpRows = kWideMaxRows / 8;  // narrow-task CTAs: each warp's sl
 struct TrsvSmem {
   double a[kWideMaxRows];
   double t[32];
-  int task, first, count, big, next;
+  int task;  // wide-stream ticket value broadcast to the CTA
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
