@@ -1,14 +1,19 @@
 // Sync-free supernodal triangular solves and the device-resident CG loop.
 //
-// factor_solve (proj/core/src/cholesky.cpp:139-168) becomes one pass of
-// 2 * nsup warp tasks: forward tasks in level order (pull: a row gathers its
-// strictly-lower entries from descendant supernodes through row lists, then
-// a dense forward solve of the diagonal block), followed by backward tasks
-// in reverse level order (gather over the panel's below-diagonal rows, then
-// a dense backward solve).  A forward task waits on its children's flags; a
-// backward task on its parent's (the root on its own forward flag).  The
-// permutation is folded into the gathers: rows read b[perm[i]] / the J
-// column perm[i], and outputs scatter to x[perm[i]].
+// factor_solve (proj/core/src/cholesky.cpp:139-168) becomes one pass over the
+// supernode tree, forward (children before parents, multifrontal: a supernode
+// sums its children's update vectors, solves its diagonal block and hands
+// L_below y to its parent) then backward (parents before children).  Three
+// kinds of work per pass (trsv_pass):
+//   * bottom levels (each >= HYKKT_TRSV_BOTTOM_MIN narrow supernodes):
+//     level-synchronous, one thread per supernode, a grid barrier per level;
+//   * wide supernodes (panel >= HYKKT_TRSV_WIDE entries): whole-CTA tasks on
+//     reserved CTAs, rows staged in shared memory;
+//   * the rest: warp tasks on warp tickets over the other CTAs.
+// Both task streams are in topological order.  y / x / update vectors are
+// their own completion flags (reset to kUnset before each pass; consumers
+// poll the value they need).  The permutation is folded into the gathers:
+// rows read b[perm[i]] / the J column perm[i], outputs scatter to x[perm[i]].
 //
 // cg_schur (solver.cpp:154-201) runs as ONE cooperative persistent kernel:
 // each iteration = [J^T p fused into the forward solve -> H^-1 -> J t +
