@@ -468,7 +468,9 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   {
     // triangular-solve task list: wide supernodes (panel >= HYKKT_TRSV_WIDE
     // entries, rows within the shared staging buffer) as CTA tasks
-    long long wide = 1024;
+    // B200 sweep: smaller trees (C1-C3) gain from more CTA tasks (256 entries),
+    // the 324k-supernode C4 tree from keeping the 48 wide CTAs to its top (1024)
+    long long wide = s.nsup <= 65536 ? 256 : 1024;
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE")) wide = std::max(1ll, std::atoll(e));
     std::vector<int> pos(std::max<idx>(1, s.nsup));
 
