@@ -196,6 +196,9 @@ struct hykkt_context {
     std::size_t fsmem = 0;
     int factor_on = 0;  // ks_factor opt-in (HYKKT_KS_FACTOR=1): correct, slower than kb_factor so far
     int prof_on = -1, prof_ctas = 0;
+    hykkt::DBuf<int> order;   // history-based longest-first system order (HYKKT_KS_LPT=0 disables)
+    long long lpt_for = -1;
+    int lpt_on = std::getenv("HYKKT_KS_LPT") ? std::atoi(std::getenv("HYKKT_KS_LPT")) : 1;
   } ks;
 
   hykkt::dev::SnPlan snplan() const {
@@ -1693,6 +1696,11 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     a.d2used = ks.d2.p;
     a.ticket = fresh_tickets(c, 1);
     a.B = B;
+    // history-based longest-first: systems in descending order of their CG
+    // iterations in the previous call on this batch (interior-method steps
+    // change the values little), so the last wave is not left with the
+    // longest systems; first call / other batch size: natural order
+    a.order = (static_cast<long long>(ks.lpt_for) == B && ks.lpt_on) ? ks.order.p : nullptr;
     if (ks.prof_on < 0) ks.prof_on = std::getenv("HYKKT_KS_PROF") ? 1 : 0;
     a.debug = std::getenv("HYKKT_KS_DEBUG") ? std::atoi(std::getenv("HYKKT_KS_DEBUG")) : 0;
     a.issuers = 4;
@@ -1731,6 +1739,13 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
     for (int b = 0; b < B; ++b) {
       cflags[b] = fl[b];
       d2used[b] = d2[b];
+    }
+    if (ks.lpt_on) {
+      std::vector<int> ord(B);
+      std::iota(ord.begin(), ord.end(), 0);
+      std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return iters[x] > iters[y]; });
+      ks.order.upload(ord, st);
+      ks.lpt_for = B;
     }
   } else {
 

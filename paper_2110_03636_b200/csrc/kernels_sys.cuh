@@ -125,6 +125,7 @@ struct KsArgs {
   int* flags;           // [B] 1 converged, 2 small quadratic
   double* d2used;       // [B]
   unsigned* ticket;     // system counter (zero on entry)
+  const int* order;     // ticket -> system (longest previous CG first), or null = identity
   int B;
   unsigned long long* prof;   // diagnostics: kPrN per CTA, or null
   unsigned long long* trace;  // diagnostics: CTA 0's first CG operator: end time per step
@@ -702,7 +703,10 @@ __global__ void __launch_bounds__(NT, 1) ks_solve(KsArgs a) {
   double* rhs = q + mc;
   bool traced = false;
   for (;;) {
-    if (tid == 0) S.sys[0] = static_cast<int>(atomicAdd(a.ticket, 1u));
+    if (tid == 0) {
+      const int t = static_cast<int>(atomicAdd(a.ticket, 1u));
+      S.sys[0] = t < a.B && a.order ? a.order[t] : t;
+    }
     __syncthreads();
     const int b = S.sys[0];
     __syncthreads();
