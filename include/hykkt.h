@@ -2,7 +2,7 @@
  * hykkt.h — C ABI of the B200-native HyKKT solve path.
  *
  * This is the drop-in boundary for the reference C++ solver API
- * (/root/reference/proj/core/include/hkkt/*.hpp).  Plain pointers and
+ * (/root/reference/proj/core/include/hkkt/ *.hpp).  Plain pointers and
  * sizes only; no torch or CUDA types.  Host arrays use the reference's
  * conventions: int64 compressed-column indices (csc_matrix.hpp:25), strictly
  * increasing rows per column, symmetric matrices as their lower triangle,
@@ -54,9 +54,10 @@ typedef struct {
   int64_t ruiz_max_iters;           /* 20    */
 } hykkt_config_t;
 
-/* Values of one block-4x4 system (hkkt::BlockKkt4x4, kkt_system.hpp:274-296)
- * on the pattern given to hykkt_analyze. Arrays are host (or, for the
- * *_device entry points, device) pointers. */
+/* Values of one block-4x4 system (hkkt::BlockKkt4x4, kkt_system.hpp:31-50)
+ * on the pattern given to hykkt_analyze.  The plain entry points accept host
+ * or device pointers (CUDA unified addressing); the *_device variants
+ * require device pointers and reject anything else. */
 typedef struct {
   const double* h_val;   /* nnz(H), lower CSC order */
   const double* j_val;   /* nnz(J) */
@@ -180,6 +181,7 @@ int hykkt_chol_analyze(hykkt_t h, int64_t n, const int64_t* colptr,
                        const int64_t* rowidx, const int64_t* perm);
 int hykkt_chol_factor(hykkt_t h, const double* values, double pivot_floor,
                       int64_t* failed_column, double* failed_pivot);
+/* Also valid on a factored KKT handle: x = H_delta^-1 b (original order). */
 int hykkt_chol_solve(hykkt_t h, const double* b, double* x);
 /* Reference-layout factor (SymbolicFactor + NumericCholesky::l_values). */
 int hykkt_chol_get_factor(hykkt_t h, int64_t* l_colptr /* n+1 */,
@@ -199,6 +201,91 @@ int hykkt_batch_solve_resident(hykkt_t h, const hykkt_config_t* cfg,
                                int flags, hykkt_report_t* reports);
 int hykkt_batch_download(hykkt_t h, double* dx, double* ds, double* dy,
                          double* dyd);
+
+/* --- device-resident values (a GPU-side interior-point
+ * method never round-trips values over PCIe).  Same layouts as the host
+ * entry points; the copies are device-to-device on the handle's stream.
+ * hykkt_solution_device / hykkt_batch_solution_device return the handle's
+ * own solution buffers (valid until the next solve or analysis; batch
+ * layout [system][entry] per field). */
+int hykkt_upload_values_device(hykkt_t h, const hykkt_values_t* values);
+int hykkt_batch_upload_device(hykkt_t h, int64_t batch, const hykkt_values_t* values);
+int hykkt_solution_device(hykkt_t h, const double** dx, const double** ds,
+                          const double** dy, const double** dyd);
+int hykkt_batch_solution_device(hykkt_t h, const double** dx, const double** ds,
+                                const double** dy, const double** dyd);
+
+/* --- Reduced2x2 path: replaces solve_reduced (solver.hpp:167-170,
+ * solver.cpp:222-293) for a caller that holds an (already scaled)
+ * hkkt::Reduced2x2 (kkt_system.hpp:56-69): H_tilde lower CSC with its full
+ * diagonal, J (m_c x n_x).  No Ruiz scaling, no recovery: dx, dy are the
+ * reduced solution; report.be_2x2 / rr_2x2 are error_report_kkt2x2 on the
+ * given system (HYKKT_FLAG_METRICS), the 4x4 fields stay NaN. */
+int hykkt_analyze_reduced(hykkt_t h, int64_t n_x, int64_t m_c,
+                          const int64_t* ht_colptr, const int64_t* ht_rowidx,
+                          const int64_t* j_colptr, const int64_t* j_rowidx,
+                          const int64_t* perm);
+int hykkt_upload_reduced(hykkt_t h, const double* ht_val, const double* j_val,
+                         const double* r_x, const double* r_y);
+int hykkt_upload_reduced_device(hykkt_t h, const double* ht_val,
+                                const double* j_val, const double* r_x,
+                                const double* r_y);
+int hykkt_solve_reduced(hykkt_t h, const hykkt_config_t* cfg,
+                        const double* ht_val, const double* j_val,
+                        const double* r_x, const double* r_y,
+                        double* delta_min_inout, int flags,
+                        hykkt_report_t* report, double* dx, double* dy);
+
+/* --- the split API of solve_reduced, phase by phase ----------------------
+ * hykkt_assemble replaces assemble_h_gamma (solver.hpp:75, solver.cpp:66-84)
+ * on the uploaded values (reduced handle: of the given Reduced2x2; block-4x4
+ * handle: of reduce() + ruiz_scale() of the system).  hg_val receives
+ * H_gamma's values on the pattern of hykkt_hgamma_pattern (nnz_h_gamma
+ * entries, the reference's add_symmetric_lower union pattern), r_hat_x the
+ * n_x right-hand side; either may be NULL (stays on the device). */
+int hykkt_assemble(hykkt_t h, const hykkt_config_t* cfg, double* hg_val,
+                   double* r_hat_x);
+int hykkt_hgamma_pattern(hykkt_t h, int64_t* colptr /* n_x+1 */,
+                         int64_t* rowidx /* nnz_h_gamma */);
+
+/* factorize_with_ladder (solver.hpp:92-94, solver.cpp:108-142): delta1 = 0,
+ * then RegularizationState::delta_min_current doubling while the pivot-free
+ * factorization fails and delta1 <= delta_max / 2; pivot floor =
+ * cfg.pivot_floor * max |diag|.  On a KKT handle `values` must be NULL (the
+ * H_gamma of the last hykkt_assemble); on a Cholesky-level handle it is the
+ * matrix in the pattern given to hykkt_chol_analyze.  *failed_column = -1 on
+ * success (the factor stays on the device for hykkt_chol_solve /
+ * hykkt_cg_schur), else the LadderFailure column; *attempts and *delta1 are
+ * RegularizationState::attempts / delta1. */
+int hykkt_factor_ladder(hykkt_t h, const hykkt_config_t* cfg,
+                        const double* values, double* delta_min_inout,
+                        int64_t* attempts, double* delta1,
+                        int64_t* failed_column);
+
+/* Loads a factor given in the reference layout (NumericCholesky::l_values on
+ * the SymbolicFactor pattern of hykkt_chol_get_factor) onto a
+ * Cholesky-level handle, so factor_solve / cg_schur can run on an L that
+ * was produced elsewhere. */
+int hykkt_chol_set_factor(hykkt_t h, const double* l_values);
+/* The constraint Jacobian J (m_c x n CSC) of SchurOperator (solver.hpp:97-103)
+ * for hykkt_cg_schur on a Cholesky-level handle. */
+int hykkt_chol_set_j(hykkt_t h, int64_t m_c, const int64_t* j_colptr,
+                     const int64_t* j_rowidx, const double* j_val);
+/* cg_schur (solver.hpp:121-122, solver.cpp:154-201) on
+ * S = J H^-1 J^T + delta2 I with the handle's factor: KKT handles use the
+ * scaled J of the last hykkt_assemble, Cholesky-level handles the J of
+ * hykkt_chol_set_j.  One persistent kernel, no host round trips; the
+ * outcome mirrors CgResult (iterations, relative_residual, converged,
+ * small_quadratic_detected). */
+int hykkt_cg_schur(hykkt_t h, const hykkt_config_t* cfg, const double* rhs,
+                   double delta2, double* x, int64_t* iterations,
+                   double* relative_residual, int32_t* converged,
+                   int32_t* small_quadratic);
+
+/* Scheduling knobs of a handle (never change results): "ks_lpt" = 1 (default)
+ * / 0 — the batched solve takes systems longest-first by the previous call's
+ * CG iteration counts / in natural order. */
+int hykkt_set_option(hykkt_t h, const char* name, int64_t value);
 
 #ifdef __cplusplus
 }

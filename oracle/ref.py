@@ -108,6 +108,12 @@ def lib() -> C.CDLL:
     L.ref_gen_get.argtypes = [vp, C.c_int64] + [I64P, I64P, F64P] * 3 + [F64P] * 6
     L.ref_cg_schur.argtypes = [C.c_int64, I64P, I64P, F64P, C.c_int64, I64P, I64P, F64P, I64P,
                                C.POINTER(RefConfig), C.c_double, F64P, F64P, I64P, F64P, I32P]
+    L.ref_reduce.argtypes = [C.POINTER(RefSystem), I64P, I64P, I64P, F64P, F64P]
+    L.ref_solve_reduced.argtypes = [C.c_int64, C.c_int64, I64P, I64P, F64P, I64P, I64P, F64P, F64P,
+                                    F64P, C.POINTER(RefConfig), I64P, F64P, C.POINTER(RefReport),
+                                    F64P, F64P]
+    L.ref_solve_sequence.argtypes = [C.c_int64, C.POINTER(RefSystem), C.POINTER(RefConfig),
+                                     C.POINTER(RefReport), F64P, I64P]
     _lib = L
     return L
 
@@ -361,3 +367,50 @@ def cg_schur(h_lower, j, rhs, cfg=None, perm=None, delta2=0.0) -> dict:
                             C.byref(fl)))
     return dict(x=x, iterations=it.value, relative_residual=rr.value,
                 converged=bool(fl.value & 1), small_quadratic=bool(fl.value & 2))
+
+
+def reduce(sys):
+    """hkkt::reduce (kkt_system.cpp:66-87) -> Reduced2x2."""
+    from paper_2110_03636_b200.kkt import CscMatrix, Reduced2x2
+    L = lib()
+    h = _SysHolder(sys)
+    nnz = C.c_int64(0)
+    _chk(L.ref_reduce(C.byref(h.s), C.byref(nnz), None, None, None, None))
+    n = sys.n_x
+    cp, ri, v, rx = np.zeros(n + 1, np.int64), np.zeros(nnz.value, np.int64), np.zeros(nnz.value), np.zeros(n)
+    _chk(L.ref_reduce(C.byref(h.s), C.byref(nnz), _ip(cp), _ip(ri), _dp(v), _dp(rx)))
+    return Reduced2x2(CscMatrix(n, n, cp, ri, v), sys.j, rx, np.array(sys.r_y, np.float64))
+
+
+def solve_reduced(red, cfg=None, perm=None, delta_min_current: float = 0.0) -> dict:
+    """hkkt::solve_reduced (solver.cpp:222-293).  perm=None: reference AMD."""
+    rc = config(cfg)
+    rep = RefReport()
+    dm = C.c_double(delta_min_current)
+    f = lambda a: np.ascontiguousarray(a, np.float64)
+    i = lambda a: np.ascontiguousarray(a, np.int64)
+    keep = [i(red.h_tilde.colptr), i(red.h_tilde.rowidx), f(red.h_tilde.values), i(red.j.colptr),
+            i(red.j.rowidx), f(red.j.values), f(red.r_x), f(red.r_y)]
+    dx, dy = np.zeros(red.n_x), np.zeros(red.m_c)
+    p = None if perm is None else i(perm)
+    _chk(lib().ref_solve_reduced(red.n_x, red.m_c, _ip(keep[0]), _ip(keep[1]), _dp(keep[2]), _ip(keep[3]),
+                                 _ip(keep[4]), _dp(keep[5]), _dp(keep[6]), _dp(keep[7]), C.byref(rc), _ip(p),
+                                 C.byref(dm), C.byref(rep), _dp(dx), _dp(dy)))
+    r = {name: getattr(rep, name) for name, _ in RefReport._fields_}
+    return dict(report=r, dx=dx, dy=dy, delta_min_current=dm.value)
+
+
+def solve_sequence(systems, cfg=None) -> dict:
+    """hkkt::solve_sequence (solver.cpp:352-412), sequential mode."""
+    rc = config(cfg)
+    holders = [_SysHolder(s) for s in systems]
+    arr = (RefSystem * len(systems))(*[h.s for h in holders])
+    reps = (RefReport * len(systems))()
+    N = systems[0].total_size
+    sols = np.zeros(len(systems) * N)
+    stats = np.zeros(4, np.int64)
+    _chk(lib().ref_solve_sequence(len(systems), arr, C.byref(rc), reps, _dp(sols), _ip(stats)))
+    return dict(reports=[{name: getattr(r, name) for name, _ in RefReport._fields_} for r in reps],
+                solutions=sols.reshape(len(systems), N),
+                stats=dict(symbolic_analyses=int(stats[0]), numeric_factorizations=int(stats[1]),
+                           factorization_attempts=int(stats[2]), pattern_uniform=bool(stats[3])))

@@ -8,8 +8,9 @@
 //
 //   solve_full          proj/core/include/hkkt/solver.hpp:182-184
 //   solve_reduced       proj/core/include/hkkt/solver.hpp:167-170
-//   reduce / ruiz_scale proj/core/include/hkkt/kkt_system.hpp:318,
-//                       proj/core/include/hkkt/ruiz.hpp:374
+//   solve_sequence      proj/core/include/hkkt/solver.hpp:204-205
+//   reduce / ruiz_scale proj/core/include/hkkt/kkt_system.hpp:76,
+//                       proj/core/include/hkkt/ruiz.hpp:48
 //   assemble_h_gamma    proj/core/include/hkkt/solver.hpp:75
 //   factorize_with_ladder  solver.hpp:92-94
 //   amd_order / symbolic_cholesky / numeric_cholesky / factor_solve
@@ -24,6 +25,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <string>
 #include <thread>
@@ -560,6 +562,87 @@ int ref_cg_schur(int64_t n, const int64_t* h_cp, const int64_t* h_ri,
     *iters = r.iterations;
     *relres = r.relative_residual;
     *flags = (r.converged ? 1 : 0) | (r.small_quadratic_detected ? 2 : 0);
+    return 0;
+  });
+}
+
+// reduce (kkt_system.cpp:66-87): H_tilde (lower CSC) and r_x of one
+// system.  Call with null outputs first to get *nnz_out.
+int ref_reduce(const RefSystem* s, int64_t* nnz_out, int64_t* ht_cp, int64_t* ht_ri,
+               double* ht_v, double* r_x) {
+  return guarded([&] {
+    const Reduced2x2 red = reduce(make_sys(s));
+    *nnz_out = red.h_tilde.nnz();
+    if (ht_cp) std::copy(red.h_tilde.col_ptr().begin(), red.h_tilde.col_ptr().end(), ht_cp);
+    if (ht_ri) std::copy(red.h_tilde.row_idx().begin(), red.h_tilde.row_idx().end(), ht_ri);
+    copy_out(red.h_tilde.values(), ht_v);
+    copy_out(red.r_x, r_x);
+    return 0;
+  });
+}
+
+// solve_reduced (solver.cpp:222-293) on an explicit Reduced2x2; perm == null:
+// the reference's own amd_order of H_gamma (a null symbolic).
+int ref_solve_reduced(int64_t n_x, int64_t m_c, const int64_t* ht_cp, const int64_t* ht_ri,
+                      const double* ht_v, const int64_t* j_cp, const int64_t* j_ri,
+                      const double* j_v, const double* r_x, const double* r_y,
+                      const RefConfig* c, const int64_t* perm, double* dmin_inout,
+                      RefReport* rep, double* dx, double* dy) {
+  return guarded([&] {
+    const SolverConfig cfg = to_cfg(c);
+    Reduced2x2 red;
+    red.h_tilde = make_csc(n_x, n_x, ht_cp, ht_ri, ht_v);
+    red.j = make_csc(m_c, n_x, j_cp, j_ri, j_v);
+    red.r_x = vec(r_x, n_x);
+    red.r_y = vec(r_y, m_c);
+    std::shared_ptr<const SymbolicFactor> sym;
+    if (perm) {
+      const HGammaSystem hg = assemble_h_gamma(red, cfg.gamma);
+      sym = std::make_shared<SymbolicFactor>(symbolic_cholesky(hg.h_gamma, make_perm(perm, n_x)));
+    }
+    RegularizationState st = RegularizationState::initial(cfg);
+    if (dmin_inout && *dmin_inout > 0.0) st.delta_min_current = *dmin_inout;
+    const ReducedSolveResult r = solve_reduced(red, cfg, sym, st);
+    if (dmin_inout) *dmin_inout = st.delta_min_current;
+    fill_report(r.report, rep);
+    if (r.ok()) {
+      copy_out(r.dx, dx);
+      copy_out(r.dy, dy);
+    }
+    return 0;
+  });
+}
+
+// solve_sequence (solver.cpp:352-412) on `count` systems: per-matrix
+// reports, solutions stacked (dx, ds, dy, dyd) per system at stride N
+// (NaN for failed ones) and stats = (symbolic_analyses,
+// numeric_factorizations, factorization_attempts, pattern_uniform).
+int ref_solve_sequence(int64_t count, const RefSystem* systems, const RefConfig* c,
+                       RefReport* reps, double* solutions, int64_t* stats) {
+  return guarded([&] {
+    const SolverConfig cfg = to_cfg(c);
+    std::vector<BlockKkt4x4> sys;
+    sys.reserve(count);
+    for (int64_t k = 0; k < count; ++k) sys.push_back(make_sys(systems + k));
+    const SequenceResult r = solve_sequence(sys, cfg);
+    for (int64_t k = 0; k < count; ++k) {
+      fill_report(r.reports[k], reps + k);
+      const int64_t N = sys[k].total_size();
+      double* out = solutions + k * N;
+      if (r.solutions[k]) {
+        const FullSolution& f = *r.solutions[k];
+        copy_out(f.dx, out);
+        copy_out(f.ds, out + f.dx.size());
+        copy_out(f.dy, out + f.dx.size() + f.ds.size());
+        copy_out(f.dyd, out + f.dx.size() + f.ds.size() + f.dy.size());
+      } else {
+        std::fill(out, out + N, std::numeric_limits<double>::quiet_NaN());
+      }
+    }
+    stats[0] = r.stats.symbolic_analyses;
+    stats[1] = r.stats.numeric_factorizations;
+    stats[2] = r.stats.factorization_attempts;
+    stats[3] = r.pattern_uniform ? 1 : 0;
     return 0;
   });
 }

@@ -86,6 +86,11 @@ EXPORTS = [
     "hykkt_last_timing", "hykkt_chol_analyze", "hykkt_chol_factor", "hykkt_chol_solve",
     "hykkt_chol_get_factor", "hykkt_batch_solve", "hykkt_batch_upload",
     "hykkt_batch_solve_resident", "hykkt_batch_download",
+    "hykkt_upload_values_device", "hykkt_batch_upload_device", "hykkt_solution_device",
+    "hykkt_batch_solution_device", "hykkt_analyze_reduced", "hykkt_upload_reduced",
+    "hykkt_upload_reduced_device", "hykkt_solve_reduced", "hykkt_assemble", "hykkt_hgamma_pattern",
+    "hykkt_factor_ladder", "hykkt_chol_set_factor", "hykkt_chol_set_j", "hykkt_cg_schur",
+    "hykkt_set_option",
 ]
 
 
@@ -141,6 +146,24 @@ def lib() -> C.CDLL:
     L.hykkt_batch_upload.argtypes = [vp, C.c_int64, C.POINTER(Values)]
     L.hykkt_batch_solve_resident.argtypes = [vp, C.POINTER(Config), C.c_int, C.POINTER(Report)]
     L.hykkt_batch_download.argtypes = [vp, F64P, F64P, F64P, F64P]
+    VPP = C.POINTER(C.c_void_p)
+    I32P = C.POINTER(C.c_int32)
+    L.hykkt_upload_values_device.argtypes = [vp, C.POINTER(Values)]
+    L.hykkt_batch_upload_device.argtypes = [vp, C.c_int64, C.POINTER(Values)]
+    L.hykkt_solution_device.argtypes = [vp, VPP, VPP, VPP, VPP]
+    L.hykkt_batch_solution_device.argtypes = [vp, VPP, VPP, VPP, VPP]
+    L.hykkt_analyze_reduced.argtypes = [vp, C.c_int64, C.c_int64, I64P, I64P, I64P, I64P, I64P]
+    L.hykkt_upload_reduced.argtypes = [vp, F64P, F64P, F64P, F64P]
+    L.hykkt_upload_reduced_device.argtypes = [vp, vp, vp, vp, vp]
+    L.hykkt_solve_reduced.argtypes = [vp, C.POINTER(Config), F64P, F64P, F64P, F64P, F64P, C.c_int,
+                                      C.POINTER(Report), F64P, F64P]
+    L.hykkt_assemble.argtypes = [vp, C.POINTER(Config), F64P, F64P]
+    L.hykkt_hgamma_pattern.argtypes = [vp, I64P, I64P]
+    L.hykkt_factor_ladder.argtypes = [vp, C.POINTER(Config), F64P, F64P, I64P, F64P, I64P]
+    L.hykkt_chol_set_factor.argtypes = [vp, F64P]
+    L.hykkt_chol_set_j.argtypes = [vp, C.c_int64, I64P, I64P, F64P]
+    L.hykkt_cg_schur.argtypes = [vp, C.POINTER(Config), F64P, C.c_double, F64P, I64P, F64P, I32P, I32P]
+    L.hykkt_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("hykkt_last_error", "hykkt_destroy", "hykkt_config_default"):

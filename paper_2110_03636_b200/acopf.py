@@ -29,6 +29,7 @@ C1-C4 (N = 10k / 40k / 200k / 1.4M).
 """
 from __future__ import annotations
 
+import functools
 import math
 
 import numpy as np
@@ -38,6 +39,7 @@ from .kkt import BlockKkt4x4, CscMatrix
 CONFIG_BUSES = {"C1": 500, "C2": 2000, "C3": 10000, "C4": 70000}
 
 
+@functools.lru_cache(maxsize=8)
 def _topology(nb: int, seed: int, branch_ratio: float):
     rng = np.random.default_rng(seed)
     w = int(math.ceil(math.sqrt(nb)))

@@ -27,7 +27,7 @@ ErrorReport error_report_2x2(const CscView& h_tilde, const CscView& j,
                              const double* r_x, const double* r_y,
                              const double* dx, const double* dy);
 
-// Block-4x4 system (kkt_system.hpp:267-270).
+// Block-4x4 system (kkt_system.hpp:22-28).
 ErrorReport error_report_4x4(const CscView& h, const CscView& j,
                              const CscView& jd, const double* d_x,
                              const double* d_s, const double* r_tilde_x,

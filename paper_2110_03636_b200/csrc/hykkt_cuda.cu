@@ -126,6 +126,12 @@ struct hykkt_context {
   bool ruiz_rows_built = false;
 
   bool have_plan = false, have_kkt = false, have_values = false, have_factor = false;
+  bool have_assembled = false;
+  // Reduced2x2 handle (hykkt_analyze_reduced): m_d = 0, D_x = 0 and identity
+  // Ruiz scaling, so the 4x4 kernels compute solve_reduced exactly
+  bool reduced = false;
+  // Cholesky-level handle with a constraint Jacobian (hykkt_chol_set_j)
+  bool have_j = false;
   hykkt::SupernodalPlan sp;
   hykkt::KktPlan kp;
 
@@ -527,6 +533,11 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   c.epoch = 0;
   c.have_plan = true;
+  // the batch buffers and completion flags belong to the previous pattern:
+  // a new hykkt_batch_upload is required, and the flags are zeroed again
+  // before the next batched factor (epochs restart at 0)
+  c.batch = 0;
+  c.bb.flags_init = false;
   c.bb.jobs_T = -1;
   c.ks.state = 0;
   c.ruiz_rows_built = false;
@@ -690,6 +701,7 @@ void validate_cfg(const hykkt_config_t& cfg) {
   if (cfg.gamma < 0.0) throw InvalidArgument("gamma must be >= 0");
   if (!(cfg.delta_min > 0.0) || !(cfg.delta_max > 0.0) || cfg.delta_min > cfg.delta_max)
     throw InvalidArgument("need 0 < delta_min <= delta_max");
+  if (!std::isfinite(cfg.delta_max)) throw InvalidArgument("delta_max must be finite (the ladder doubles up to it)");
   if (cfg.delta2 < 0.0) throw InvalidArgument("delta2 must be >= 0");
   if (!(cfg.cg_tol > 0.0)) throw InvalidArgument("cg_tol must be positive");
   if (cfg.cg_max_iter <= 0) throw InvalidArgument("cg_max_iter must be > 0");
@@ -797,29 +809,64 @@ void analyze_kkt(Ctx& c, idx nx, idx mc, idx md, const std::int64_t* hcp, const 
   CK(cudaStreamSynchronize(st));
   c.have_kkt = true;
   c.have_values = false;
+  c.have_assembled = false;
+  c.reduced = false;
+  c.have_j = true;
 }
 
-void upload_values(Ctx& c, const hykkt_values_t* v) {
+// Host or device source (UVA: cudaMemcpyDefault); `device_only` rejects
+// anything but device memory (the *_device entry points).
+void copy_in(double* dst, const double* src, idx n, const char* name, cudaStream_t st, bool device_only) {
+  if (n <= 0) return;
+  if (!src) throw InvalidArgument(std::string("null ") + name);
+  if (device_only) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, src) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      throw InvalidArgument(std::string(name) + " is not a device pointer");
+    }
+  }
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, st));
+}
+
+void upload_values(Ctx& c, const hykkt_values_t* v, bool device_only = false) {
   if (!c.have_kkt) throw StateError("hykkt_analyze must be called first");
+  if (c.reduced) throw StateError("reduced handle: use hykkt_upload_reduced");
   if (!v) throw InvalidArgument("null values");
   const KktPlan& k = c.kp;
   cudaStream_t st = c.stream;
-  auto up = [&](hykkt::DBuf<double>& b, const double* src, idx n, const char* name) {
-    if (n > 0 && !src) throw InvalidArgument(std::string("null ") + name);
-    if (n > 0) CK(cudaMemcpyAsync(b.p, src, n * sizeof(double), cudaMemcpyHostToDevice, st));
-  };
-  up(c.hval, v->h_val, k.h.nnz(), "h_val");
-  up(c.jval, v->j_val, k.j.nnz(), "j_val");
-  up(c.jdval, v->jd_val, k.jd.nnz(), "jd_val");
-  up(c.d_x, v->d_x, k.nx, "d_x");
-  up(c.d_s, v->d_s, k.md, "d_s");
-  up(c.r_tx, v->r_tilde_x, k.nx, "r_tilde_x");
-  up(c.r_s, v->r_s, k.md, "r_s");
-  up(c.r_y, v->r_y, k.mc, "r_y");
-  up(c.r_yd, v->r_yd, k.md, "r_yd");
+  copy_in(c.hval.p, v->h_val, k.h.nnz(), "h_val", st, device_only);
+  copy_in(c.jval.p, v->j_val, k.j.nnz(), "j_val", st, device_only);
+  copy_in(c.jdval.p, v->jd_val, k.jd.nnz(), "jd_val", st, device_only);
+  copy_in(c.d_x.p, v->d_x, k.nx, "d_x", st, device_only);
+  copy_in(c.d_s.p, v->d_s, k.md, "d_s", st, device_only);
+  copy_in(c.r_tx.p, v->r_tilde_x, k.nx, "r_tilde_x", st, device_only);
+  copy_in(c.r_s.p, v->r_s, k.md, "r_s", st, device_only);
+  copy_in(c.r_y.p, v->r_y, k.mc, "r_y", st, device_only);
+  copy_in(c.r_yd.p, v->r_yd, k.md, "r_yd", st, device_only);
   c.v = {c.hval.p, c.jval.p, c.jdval.p, c.d_x.p, c.d_s.p, c.r_tx.p, c.r_s.p, c.r_y.p, c.r_yd.p};
   c.o = {c.dx.p, c.dy.p, c.ds.p, c.dyd.p};
   c.have_values = true;
+  c.have_assembled = false;
+}
+
+// Reduced2x2 values (kkt_system.hpp:56-69): H_tilde on the analysed lower
+// pattern, J, r_x, r_y.  D_x = 0 and no J_d, so reduce() returns H_tilde
+// and r_x unchanged.
+void upload_reduced(Ctx& c, const double* ht, const double* j, const double* rx, const double* ry,
+                    bool device_only = false) {
+  if (!c.have_kkt || !c.reduced) throw StateError("hykkt_analyze_reduced must be called first");
+  const KktPlan& k = c.kp;
+  cudaStream_t st = c.stream;
+  copy_in(c.hval.p, ht, k.h.nnz(), "h_tilde values", st, device_only);
+  copy_in(c.jval.p, j, k.j.nnz(), "j values", st, device_only);
+  copy_in(c.r_tx.p, rx, k.nx, "r_x", st, device_only);
+  copy_in(c.r_y.p, ry, k.mc, "r_y", st, device_only);
+  if (k.nx > 0) CK(cudaMemsetAsync(c.d_x.p, 0, k.nx * sizeof(double), st));
+  c.v = {c.hval.p, c.jval.p, c.jdval.p, c.d_x.p, c.d_s.p, c.r_tx.p, c.r_s.p, c.r_y.p, c.r_yd.p};
+  c.o = {c.dx.p, c.dy.p, c.ds.p, c.dyd.p};
+  c.have_values = true;
+  c.have_assembled = false;
 }
 
 struct Events {
@@ -837,41 +884,34 @@ struct Events {
   }
 };
 
-void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int flags,
-                    hykkt_report_t* rep) {
+// ---- solve_full / solve_reduced in phases (solver.cpp:222-328) ------------
+// Each phase is also reachable on its own through the C ABI
+// (hykkt_assemble, hykkt_factor_ladder, hykkt_cg_schur), so a caller of the
+// reference's split API (assemble_h_gamma -> factorize_with_ladder ->
+// factor_solve / cg_schur) drives the same device code as solve_full.
+
+// reduce -> ruiz_scale (identity for the Reduced2x2 entry points) -> scale
+// -> assemble_h_gamma.  Returns the Ruiz sweep count (0 for reduced handles).
+void assemble_phase(Ctx& c, const hykkt_config_t& cfg) {
   if (!c.have_values) throw StateError("no values uploaded");
-  validate_cfg(cfg);
-  const KktPlan& k = c.kp;
   const dev::AsmPlan ap = c.asmplan();
   cudaStream_t st = c.stream;
-  const long long launches0 = c.launches;
-  Events ev;
-  if (flags & HYKKT_FLAG_TIMING) ev.create();
-  hykkt_report_t r{};
-  const double nan = std::numeric_limits<double>::quiet_NaN();
-  r.be_4x4 = r.rr_4x4 = r.be_2x2 = r.rr_2x2 = r.be_2x2_scaled = r.rr_2x2_scaled = nan;
-  r.failed_column = -1;
-  r.symbolic_reused = 0;
-  // density_report (metrics.cpp:242-255) on the reduced pattern.
-  {
-    const idx hdiag = k.nx;  // H_tilde always stores the full diagonal
-    const idx hfull = 2 * (k.ht.nnz() - hdiag) + hdiag;
-    r.nnz_op = hfull + 2 * k.j.nnz() + k.nx;
-    r.nnz_fac = 2 * c.sp.l_nnz();
-    r.density_ratio = r.nnz_op > 0 ? static_cast<double>(r.nnz_fac) / r.nnz_op : 0.0;
-    r.rho_c = k.nx > 0 ? static_cast<double>(r.nnz_fac) / k.nx : 0.0;
-  }
-
-  ev.rec(0, st);
-  // ---- assembly: reduce, Ruiz, scale, H_gamma -------------------------
   const long long nred = std::max<long long>(ap.n_ht, ap.nx);
   dev::k_reduce<<<blocks_for(nred), kThreads, 0, st>>>(ap, c.v.h, c.v.jd, c.v.dx, c.v.ds,
                                                        c.v.rtx, c.v.rs, c.v.ryd, c.ht.p, c.r_x.p);
   check_launch(c);
-  c.ruiz_flags.alloc(cfg.ruiz_max_iters + 2);
-  CK(cudaMemsetAsync(c.ruiz_flags.p, 0, sizeof(int) * (cfg.ruiz_max_iters + 2), st));
   CK(cudaMemsetAsync(&c.status.p->abort, 0, sizeof(int), st));
-  {
+  if (c.reduced) {
+    // solve_reduced takes an already scaled Reduced2x2: D = I (x * 1 = x exactly)
+    const int nd = static_cast<int>(ap.nx + ap.mc);
+    if (nd > 0) {
+      dev::k_fill<<<blocks_for(nd), kThreads, 0, st>>>(c.dscale.p, nd, 1.0);
+      check_launch(c);
+    }
+    CK(cudaMemsetAsync(&c.status.p->ruiz_sweeps, 0, sizeof(int), st));
+  } else {
+    c.ruiz_flags.alloc(cfg.ruiz_max_iters + 2);
+    CK(cudaMemsetAsync(c.ruiz_flags.p, 0, sizeof(int) * (cfg.ruiz_max_iters + 2), st));
     dev::RuizArgs ra;
     ra.p = ap;
     ra.ht = c.ht.p;
@@ -895,87 +935,151 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
   dev::k_hgamma<<<blocks_for(nhg), kThreads, 0, st>>>(ap, cfg.gamma, c.hts.p, c.js.p, c.rxs.p, c.rys.p,
                                                       c.hg.p, c.rhat.p, c.maxdiag.p);
   check_launch(c);
-  ev.rec(1, st);
+  c.have_assembled = true;
+  c.have_factor = false;
+}
 
-  // ---- delta1 ladder (solver.cpp:108-142) --------------------------------
-  double dmin = (dmin_inout && *dmin_inout > 0.0) ? *dmin_inout : cfg.delta_min;
-  double delta1 = 0.0;
+struct LadderOut {
   int attempts = 0;
+  double delta1 = 0.0;
+  long long failed = -1;  // failed elimination column of the last attempt, -1 on success
+};
+
+// factorize_with_ladder (solver.cpp:108-142) on the H_gamma values `src`
+// (slots of the analysed pattern) with the pivot floor relative to
+// max |diag| in `maxdiag`: delta1 = 0, then delta_min_current doubling while
+// the attempt fails and delta1 <= delta_max / 2.  *dmin_inout carries
+// RegularizationState::delta_min_current (<= 0: cfg.delta_min).
+LadderOut ladder_phase(Ctx& c, const hykkt_config_t& cfg, const double* src, const double* maxdiag,
+                       double* dmin_inout) {
+  LadderOut o;
+  double dmin = (dmin_inout && *dmin_inout > 0.0) ? *dmin_inout : cfg.delta_min;
   auto attempt = [&](double d1) {
-    ++attempts;
-    return factor_attempt(c, c.hg.p, d1, 0.0, c.maxdiag.p, cfg.pivot_floor);
+    ++o.attempts;
+    return factor_attempt(c, src, d1, 0.0, maxdiag, cfg.pivot_floor);
   };
   int failed = attempt(0.0);
-  while (failed >= 0 && delta1 <= cfg.delta_max / 2.0) {
-    if (delta1 == 0.0) {
-      delta1 = dmin;
+  while (failed >= 0 && o.delta1 <= cfg.delta_max / 2.0) {
+    if (o.delta1 == 0.0) {
+      o.delta1 = dmin;
     } else {
       dmin *= 2.0;
-      delta1 = dmin;
+      o.delta1 = dmin;
     }
-    failed = attempt(delta1);
+    failed = attempt(o.delta1);
   }
   if (dmin_inout) *dmin_inout = dmin;
-  r.factorization_attempts = attempts;
-  r.delta1_final = delta1;
+  o.failed = failed;
+  c.have_factor = failed < 0;
+  return o;
+}
+
+struct CgOut {
+  dev::CgResultDev cg{};
+  double delta2_used = 0.0;
+  long long launches = 0;
+};
+
+// cg_schur with the delta2 restart of solve_reduced (solver.cpp:257-264) on
+// the rhs already in c.cg_rhs; the solution stays in c.cg_x.
+CgOut cg_phase(Ctx& c, const hykkt_config_t& cfg) {
+  CgOut o;
+  const long long cg0 = c.launches;
+  o.cg = run_cg(c, cfg, 0.0);
+  if (o.cg.small_quadratic) {
+    o.cg = run_cg(c, cfg, cfg.delta2);
+    o.delta2_used = cfg.delta2;
+  }
+  o.launches = c.launches - cg0;
+  return o;
+}
+
+// w = H^-1 r_hat_x; Schur rhs = J w - r_y (solver.cpp:252-255).
+void w_phase(Ctx& c) {
+  run_trsv(c, c.rhat.p, nullptr, c.js.p, nullptr);
+  if (c.kp.mc > 0) {
+    dev::k_schur_rhs<<<blocks_for(c.kp.mc), kThreads, 0, c.stream>>>(
+        static_cast<int>(c.kp.mc), c.jcsr_rp.p, c.jcsr_ci_perm.p, c.js_csr.p, c.xsol.p, c.rys.p, c.cg_rhs.p);
+    check_launch(c);
+  }
+}
+
+// dx = H^-1 (r_hat_x - J^T dy) (solver.cpp:276-281); unscale; recover.
+void dx_phase(Ctx& c) {
+  const KktPlan& k = c.kp;
+  const dev::AsmPlan ap = c.asmplan();
+  run_trsv(c, c.rhat.p, c.cg_x.p, c.js.p, c.dx_s.p);
+  const long long nrec = std::max<long long>({(long long)k.nx, (long long)k.mc, (long long)k.md});
+  dev::k_recover<<<blocks_for(nrec), kThreads, 0, c.stream>>>(ap, c.jdcsr_rp.p, c.jdcsr_ci.p, c.jdcsr_src.p,
+                                                             c.dscale.p, c.dx_s.p, c.cg_x.p, c.v.jd, c.v.ds,
+                                                             c.v.rs, c.v.ryd, c.o.dx, c.o.dy, c.o.ds, c.o.dyd);
+  check_launch(c);
+}
+
+// density_report (metrics.cpp:242-255) on the reduced pattern.
+void density_fields(const Ctx& c, hykkt_report_t& r) {
+  const KktPlan& k = c.kp;
+  const idx hdiag = k.nx;  // H_tilde always stores the full diagonal
+  const idx hfull = 2 * (k.ht.nnz() - hdiag) + hdiag;
+  r.nnz_op = hfull + 2 * k.j.nnz() + k.nx;
+  r.nnz_fac = 2 * c.sp.l_nnz();
+  r.density_ratio = r.nnz_op > 0 ? static_cast<double>(r.nnz_fac) / r.nnz_op : 0.0;
+  r.rho_c = k.nx > 0 ? static_cast<double>(r.nnz_fac) / k.nx : 0.0;
+}
+
+void metrics_phase(Ctx& c, hykkt_report_t& r);
+
+void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int flags,
+                    hykkt_report_t* rep) {
+  if (!c.have_values) throw StateError("no values uploaded");
+  validate_cfg(cfg);
+  cudaStream_t st = c.stream;
+  const long long launches0 = c.launches;
+  Events ev;
+  if (flags & HYKKT_FLAG_TIMING) ev.create();
+  hykkt_report_t r{};
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  r.be_4x4 = r.rr_4x4 = r.be_2x2 = r.rr_2x2 = r.be_2x2_scaled = r.rr_2x2_scaled = nan;
+  r.failed_column = -1;
+  r.symbolic_reused = 0;
+  density_fields(c, r);
+  c.timing = hykkt_timing_t{};
+
+  ev.rec(0, st);
+  assemble_phase(c, cfg);
+  ev.rec(1, st);
+  const LadderOut lo = ladder_phase(c, cfg, c.hg.p, c.maxdiag.p, dmin_inout);
+  r.factorization_attempts = lo.attempts;
+  r.delta1_final = lo.delta1;
   {
     StatusBlock sb;
     CK(cudaMemcpy(&sb, c.status.p, sizeof(sb), cudaMemcpyDeviceToHost));
     r.ruiz_iterations = sb.ruiz_sweeps;
   }
   ev.rec(2, st);
-  if (failed >= 0) {
+  if (lo.failed >= 0) {
     r.status = 2;  // kFailedDeltaMaxExceeded
-    r.failed_column = failed;
-    c.have_factor = false;
+    r.failed_column = lo.failed;
     if (rep) *rep = r;
-    c.timing = hykkt_timing_t{};
     c.timing.kernel_launches = c.launches - launches0;
     return;
   }
-  c.have_factor = true;
-
-  // ---- w = H^-1 r_hat_x, Schur rhs = J w - r_y ----------------------------
-  run_trsv(c, c.rhat.p, nullptr, c.js.p, nullptr);
-  if (k.mc > 0) {
-    dev::k_schur_rhs<<<blocks_for(k.mc), kThreads, 0, st>>>(static_cast<int>(k.mc), c.jcsr_rp.p, c.jcsr_ci_perm.p,
-                                                           c.js_csr.p, c.xsol.p, c.rys.p, c.cg_rhs.p);
-    check_launch(c);
-  }
+  w_phase(c);
   ev.rec(3, st);
-
-  // ---- CG with the delta2 restart (solver.cpp:257-264) --------------------
-  const long long cg0 = c.launches;
-  dev::CgResultDev cg = run_cg(c, cfg, 0.0);
-  double delta2_used = 0.0;
-  if (cg.small_quadratic) {
-    cg = run_cg(c, cfg, cfg.delta2);
-    delta2_used = cfg.delta2;
-  }
-  const long long cg_launches = c.launches - cg0;
-  r.delta2_used = delta2_used;
-  r.cg_iterations = cg.iterations;
-  r.cg_relative_residual = cg.relres;
+  const CgOut co = cg_phase(c, cfg);
+  r.delta2_used = co.delta2_used;
+  r.cg_iterations = co.cg.iterations;
+  r.cg_relative_residual = co.cg.relres;
   ev.rec(4, st);
-  if (!cg.converged) {
+  if (!co.cg.converged) {
     r.status = 3;  // kFailedCgNoConvergence
     if (rep) *rep = r;
-    c.timing = hykkt_timing_t{};
     c.timing.kernel_launches = c.launches - launches0;
-    c.timing.cg_kernel_launches = cg_launches;
+    c.timing.cg_kernel_launches = co.launches;
     return;
   }
-  r.status = delta2_used > 0.0 ? 1 : 0;
-
-  // ---- dx = H^-1 (r_hat_x - J^T dy); unscale; recover ---------------------
-  run_trsv(c, c.rhat.p, c.cg_x.p, c.js.p, c.dx_s.p);
-  {
-    const long long nrec = std::max<long long>({(long long)k.nx, (long long)k.mc, (long long)k.md});
-    dev::k_recover<<<blocks_for(nrec), kThreads, 0, st>>>(ap, c.jdcsr_rp.p, c.jdcsr_ci.p, c.jdcsr_src.p, c.dscale.p,
-                                                          c.dx_s.p, c.cg_x.p, c.v.jd, c.v.ds, c.v.rs, c.v.ryd,
-                                                          c.o.dx, c.o.dy, c.o.ds, c.o.dyd);
-    check_launch(c);
-  }
+  r.status = co.delta2_used > 0.0 ? 1 : 0;
+  dx_phase(c);
   ev.rec(5, st);
   CK(cudaStreamSynchronize(st));
   {
@@ -983,7 +1087,6 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
     CK(cudaMemcpy(&sb, c.status.p, sizeof(sb), cudaMemcpyDeviceToHost));
     if (sb.abort) throw TimeoutError("device wait timed out in the dx solve");
   }
-  c.timing = hykkt_timing_t{};
   if (ev.on) {
     float ms[5];
     for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev.e[i], ev.e[i + 1]));
@@ -997,46 +1100,52 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
     c.timing.total_ms = tot;
   }
   c.timing.kernel_launches = c.launches - launches0;
-  c.timing.cg_kernel_launches = cg_launches;
+  c.timing.cg_kernel_launches = co.launches;
+  if (flags & HYKKT_FLAG_METRICS) metrics_phase(c, r);
+  if (rep) *rep = r;
+}
 
-  if (flags & HYKKT_FLAG_METRICS) {
-    const idx nx = k.nx, mc = k.mc, md = k.md;
-    auto dl = [&](const double* src, idx n) {
-      std::vector<double> h(n);
-      if (n) CK(cudaMemcpy(h.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost));
-      return h;
-    };
-    const auto hv = dl(c.v.h, k.h.nnz()), jv = dl(c.v.j, k.j.nnz()), jdv = dl(c.v.jd, k.jd.nnz());
-    const auto dxv = dl(c.v.dx, nx), dsv = dl(c.v.ds, md), rtx = dl(c.v.rtx, nx), rs = dl(c.v.rs, md),
-               ry = dl(c.v.ry, mc), ryd = dl(c.v.ryd, md);
-    const auto htv = dl(c.ht.p, k.ht.nnz()), htsv = dl(c.hts.p, k.ht.nnz()), jsv = dl(c.js.p, k.j.nnz());
-    const auto rx = dl(c.r_x.p, nx), rxs = dl(c.rxs.p, nx), rys = dl(c.rys.p, mc);
-    const auto sdx = dl(c.dx_s.p, nx), sdy = dl(c.cg_x.p, mc);
-    const auto odx = dl(c.o.dx, nx), ody = dl(c.o.dy, mc), ods = dl(c.o.ds, md), odyd = dl(c.o.dyd, md);
-    const CscView H{nx, nx, k.h.cp.data(), k.h.ri.data(), hv.data()};
-    const CscView J{mc, nx, k.j.cp.data(), k.j.ri.data(), jv.data()};
-    const CscView JD{md, nx, k.jd.cp.data(), k.jd.ri.data(), jdv.data()};
-    const CscView HT{nx, nx, k.ht.cp.data(), k.ht.ri.data(), htv.data()};
-    const CscView HTS{nx, nx, k.ht.cp.data(), k.ht.ri.data(), htsv.data()};
-    const CscView JS{mc, nx, k.j.cp.data(), k.j.ri.data(), jsv.data()};
-    const ErrorReport e2s = error_report_2x2(HTS, JS, rxs.data(), rys.data(), sdx.data(), sdy.data());
-    const ErrorReport e2 = error_report_2x2(HT, J, rx.data(), ry.data(), odx.data(), ody.data());
+// BE / RR of the 2x2 scaled, 2x2 and 4x4 systems (metrics.cpp:28-240) on
+// the host from the downloaded solution (outside the device path).
+void metrics_phase(Ctx& c, hykkt_report_t& r) {
+  const KktPlan& k = c.kp;
+  const idx nx = k.nx, mc = k.mc, md = k.md;
+  auto dl = [&](const double* src, idx n) {
+    std::vector<double> h(n);
+    if (n) CK(cudaMemcpy(h.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost));
+    return h;
+  };
+  const auto hv = dl(c.v.h, k.h.nnz()), jv = dl(c.v.j, k.j.nnz()), jdv = dl(c.v.jd, k.jd.nnz());
+  const auto dxv = dl(c.v.dx, nx), dsv = dl(c.v.ds, md), rtx = dl(c.v.rtx, nx), rs = dl(c.v.rs, md),
+             ry = dl(c.v.ry, mc), ryd = dl(c.v.ryd, md);
+  const auto htv = dl(c.ht.p, k.ht.nnz()), htsv = dl(c.hts.p, k.ht.nnz()), jsv = dl(c.js.p, k.j.nnz());
+  const auto rx = dl(c.r_x.p, nx), rxs = dl(c.rxs.p, nx), rys = dl(c.rys.p, mc);
+  const auto sdx = dl(c.dx_s.p, nx), sdy = dl(c.cg_x.p, mc);
+  const auto odx = dl(c.o.dx, nx), ody = dl(c.o.dy, mc), ods = dl(c.o.ds, md), odyd = dl(c.o.dyd, md);
+  const CscView H{nx, nx, k.h.cp.data(), k.h.ri.data(), hv.data()};
+  const CscView J{mc, nx, k.j.cp.data(), k.j.ri.data(), jv.data()};
+  const CscView JD{md, nx, k.jd.cp.data(), k.jd.ri.data(), jdv.data()};
+  const CscView HT{nx, nx, k.ht.cp.data(), k.ht.ri.data(), htv.data()};
+  const CscView HTS{nx, nx, k.ht.cp.data(), k.ht.ri.data(), htsv.data()};
+  const CscView JS{mc, nx, k.j.cp.data(), k.j.ri.data(), jsv.data()};
+  const ErrorReport e2s = error_report_2x2(HTS, JS, rxs.data(), rys.data(), sdx.data(), sdy.data());
+  const ErrorReport e2 = error_report_2x2(HT, J, rx.data(), ry.data(), odx.data(), ody.data());
+  r.be_2x2_scaled = e2s.be;
+  r.rr_2x2_scaled = e2s.rr;
+  r.be_2x2 = e2.be;
+  r.rr_2x2 = e2.rr;
+  if (!c.reduced) {
     const ErrorReport e4 = error_report_4x4(H, J, JD, dxv.data(), dsv.data(), rtx.data(), rs.data(), ry.data(),
                                             ryd.data(), odx.data(), ods.data(), ody.data(), odyd.data());
-    r.be_2x2_scaled = e2s.be;
-    r.rr_2x2_scaled = e2s.rr;
-    r.be_2x2 = e2.be;
-    r.rr_2x2 = e2.rr;
     r.be_4x4 = e4.be;
     r.rr_4x4 = e4.rr;
   }
-  if (rep) *rep = r;
 }
 
 void download_solution(Ctx& c, double* dx, double* ds, double* dy, double* dyd) {
   const KktPlan& k = c.kp;
   auto dl = [&](const double* src, double* out, idx n) {
-    if (out && n) CK(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    if (out && n) CK(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDefault, c.stream));
   };
   dl(c.o.dx, dx, k.nx);
   dl(c.o.ds, ds, k.md);
@@ -1069,8 +1178,9 @@ BatchLayout batch_layout(const KktPlan& k) {
 int pow2_at_least(long long v);
 void batch_interleave_inputs(Ctx& c);
 
-void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v) {
+void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v, bool device_only = false) {
   if (!c.have_kkt) throw StateError("hykkt_analyze must be called first");
+  if (c.reduced) throw StateError("the batched path takes block-4x4 systems (hykkt_analyze)");
   if (batch <= 0) throw InvalidArgument("batch must be positive");
   if (!v) throw InvalidArgument("null values");
   const BatchLayout L = batch_layout(c.kp);
@@ -1079,8 +1189,7 @@ void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v) {
   idx off = 0;
   for (int i = 0; i < 9; ++i) {
     const idx n = batch * L.sizes[i];
-    if (n > 0 && !src[i]) throw InvalidArgument("null value array in batch upload");
-    if (n > 0) CK(cudaMemcpyAsync(c.bvals.p + off, src[i], n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    copy_in(c.bvals.p + off, src[i], n, "batch value array", c.stream, device_only);
     off += n;
   }
   const idx nout = c.kp.nx + c.kp.mc + 2 * c.kp.md;
@@ -1422,8 +1531,13 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
   bb.sweeps.alloc(Bp); bb.delta1.alloc(Bp); bb.active.alloc(Bp); bb.fail.alloc(Bp);
   bb.running.alloc(Bp); bb.start.alloc(Bp); bb.flags.alloc(Bp); bb.iters.alloc(Bp); bb.relres.alloc(Bp);
   bb.live.alloc(cfg.cg_max_iter + 2);
-  bb.fac_done.alloc(std::max<idx>(1, sp.nsup) * T); bb.fdone.alloc(std::max<idx>(1, sp.nsup) * T);
-  bb.bdone.alloc(std::max<idx>(1, sp.nsup) * T);
+  {
+    // a reallocated flag array holds garbage: zero it again
+    const int* before[3] = {bb.fac_done.p, bb.fdone.p, bb.bdone.p};
+    bb.fac_done.alloc(std::max<idx>(1, sp.nsup) * T); bb.fdone.alloc(std::max<idx>(1, sp.nsup) * T);
+    bb.bdone.alloc(std::max<idx>(1, sp.nsup) * T);
+    if (before[0] != bb.fac_done.p || before[1] != bb.fdone.p || before[2] != bb.bdone.p) bb.flags_init = false;
+  }
   if (!bb.flags_init) {
     CK(cudaMemsetAsync(bb.fac_done.p, 0, bb.fac_done.n * sizeof(int), st));
     CK(cudaMemsetAsync(bb.fdone.p, 0, bb.fdone.n * sizeof(int), st));
@@ -1494,7 +1608,9 @@ void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_re
       check_launch(c);
     }
   }
-  for (int round = 0; round < 64; ++round) {
+  // every round doubles each active system's delta1 until it exceeds
+  // delta_max / 2 (solver.cpp:108-142), so the loop ends without a cap
+  for (;;) {
     bool any = false;
     for (int b = 0; b < Bp; ++b) any = any || act[b];
     if (!any) break;
@@ -1930,7 +2046,7 @@ void batch_download(Ctx& c, double* dx, double* ds, double* dy, double* dyd) {
   const KktPlan& k = c.kp;
   const idx B = c.batch;
   auto dl = [&](const double* src, double* out, idx n) {
-    if (out && n) CK(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    if (out && n) CK(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDefault, c.stream));
   };
   const double* o = c.bouts.p;
   dl(o, dx, B * k.nx);
@@ -2252,6 +2368,10 @@ int hykkt_chol_analyze(hykkt_t h, int64_t n, const int64_t* colptr, const int64_
     std::vector<idx> pv;
     if (perm) pv.assign(perm, perm + n);
     c.have_kkt = false;
+    c.have_values = false;
+    c.have_assembled = false;
+    c.reduced = false;
+    c.have_j = false;
     c.kp = KktPlan{};
     c.kp.hg = a;  // source pattern for scatter bookkeeping
     c.sp = build_supernodal_plan(a, std::move(pv));
@@ -2291,10 +2411,10 @@ int hykkt_chol_solve(hykkt_t h, const double* b, double* x) {
     const idx n = c.sp.n;
     if (n == 0) return;
     if (!b || !x) throw InvalidArgument("null vector");
-    CK(cudaMemcpyAsync(c.bvec.p, b, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaMemcpyAsync(c.bvec.p, b, n * sizeof(double), cudaMemcpyDefault, c.stream));
     CK(cudaMemsetAsync(&c.status.p->abort, 0, sizeof(int), c.stream));
     run_trsv(c, c.bvec.p, nullptr, nullptr, c.xvec.p);
-    CK(cudaMemcpyAsync(x, c.xvec.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(x, c.xvec.p, n * sizeof(double), cudaMemcpyDefault, c.stream));
     read_status(c);
   });
 }
@@ -2444,6 +2564,265 @@ int hykkt_batch_solve(hykkt_t h, const hykkt_config_t* cfg, int64_t batch, const
     batch_upload(c, batch, values);
     batch_solve_resident(c, cfg ? *cfg : d, flags, reports);
     batch_download(c, dx, ds, dy, dyd);
+  });
+}
+
+}  // extern "C"
+
+// ---- the split reference API (solver.hpp:75, :92-94, :121-122, :167-170) ----
+namespace hykkt {
+namespace {
+
+void require_factor(const Ctx& c) {
+  if (!c.have_factor) throw StateError("no successful factorization on this handle");
+}
+
+// Reference-layout L values (SymbolicFactor::l_col_ptr order) into the
+// supernodal panels: the inverse of hykkt_chol_get_factor.
+void set_factor(Ctx& c, const double* l_values) {
+  if (!c.have_plan) throw StateError("no analysis");
+  const SupernodalPlan& s = c.sp;
+  if (!l_values && !s.l_to_panel.empty()) throw InvalidArgument("null l_values");
+  std::vector<double> pan(std::max<idx>(1, s.panel_size), 0.0);
+  for (std::size_t q = 0; q < s.l_to_panel.size(); ++q) pan[s.l_to_panel[q]] = l_values[q];
+  CK(cudaMemcpyAsync(c.panel.p, pan.data(), s.panel_size * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  c.have_factor = true;
+}
+
+// J (m_c x n, CSC) for hykkt_cg_schur on a Cholesky-level handle: CSC for the
+// J^T gathers of the forward solve, CSR (ascending columns, the reference's
+// spmv scatter order, csc_matrix.cpp:250-254) for J t.
+void chol_set_j(Ctx& c, idx mc, const std::int64_t* cp, const std::int64_t* ri, const double* val) {
+  if (!c.have_plan || c.have_kkt) throw StateError("hykkt_chol_set_j needs a Cholesky-level handle");
+  if (mc < 0) throw InvalidArgument("negative m_c");
+  const idx n = c.sp.n;
+  CscPattern j = pattern_from(mc, n, cp, ri);
+  const idx nnz = j.nnz();
+  if (nnz > 0 && !val) throw InvalidArgument("null J values");
+  for (idx q = 0; q < nnz; ++q) {
+    if (j.ri[q] < 0 || j.ri[q] >= mc) throw InvalidArgument("J row index out of range");
+  }
+  std::vector<int> rp(mc + 1, 0), ci(std::max<idx>(nnz, 1)), cip(std::max<idx>(nnz, 1));
+  std::vector<double> vcsr(std::max<idx>(nnz, 1));
+  for (idx q = 0; q < nnz; ++q) rp[j.ri[q] + 1]++;
+  std::partial_sum(rp.begin(), rp.end(), rp.begin());
+  std::vector<int> cur(rp.begin(), rp.end() - 1);
+  for (idx col = 0; col < n; ++col) {
+    for (idx q = j.cp[col]; q < j.cp[col + 1]; ++q) {
+      const int e = cur[j.ri[q]]++;
+      cip[e] = static_cast<int>(c.sp.iperm[col]);
+      vcsr[e] = val[q];
+    }
+  }
+  cudaStream_t st = c.stream;
+  c.kp.mc = mc;
+  c.j_cp.upload(to_i32(j.cp), st);
+  c.j_ri.upload(to_i32(j.ri), st);
+  c.js.alloc(std::max<idx>(nnz, 1));
+  if (nnz) CK(cudaMemcpyAsync(c.js.p, val, nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+  c.jcsr_rp.upload(rp, st);
+  c.jcsr_ci_perm.upload(cip, st);
+  c.js_csr.upload(vcsr, st);
+  c.cg_rhs.alloc(std::max<idx>(mc, 1));
+  c.cg_x.alloc(std::max<idx>(mc, 1));
+  c.cg_r.alloc(std::max<idx>(mc, 1));
+  c.cg_p.alloc(std::max<idx>(mc, 1));
+  c.cg_q.alloc(std::max<idx>(mc, 1));
+  c.partials.alloc(4 * static_cast<std::size_t>(std::max(c.coop_cg_blocks, 1)));
+  CK(cudaStreamSynchronize(st));
+  c.have_j = true;
+}
+
+}  // namespace
+}  // namespace hykkt
+
+extern "C" {
+
+int hykkt_analyze_reduced(hykkt_t h, int64_t n_x, int64_t m_c, const int64_t* ht_colptr,
+                          const int64_t* ht_rowidx, const int64_t* j_colptr, const int64_t* j_rowidx,
+                          const int64_t* perm) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (n_x < 0) throw InvalidArgument("negative dimension");
+    const std::vector<int64_t> jd_cp(static_cast<std::size_t>(n_x) + 1, 0);
+    analyze_kkt(c, n_x, m_c, 0, ht_colptr, ht_rowidx, j_colptr, j_rowidx, jd_cp.data(), nullptr, perm);
+    c.reduced = true;
+  });
+}
+
+int hykkt_upload_reduced(hykkt_t h, const double* ht_val, const double* j_val, const double* r_x,
+                         const double* r_y) {
+  return guarded([&] { upload_reduced(ctx(h), ht_val, j_val, r_x, r_y); });
+}
+
+int hykkt_upload_reduced_device(hykkt_t h, const double* ht_val, const double* j_val, const double* r_x,
+                                const double* r_y) {
+  return guarded([&] { upload_reduced(ctx(h), ht_val, j_val, r_x, r_y, true); });
+}
+
+int hykkt_solve_reduced(hykkt_t h, const hykkt_config_t* cfg, const double* ht_val, const double* j_val,
+                        const double* r_x, const double* r_y, double* delta_min_inout, int flags,
+                        hykkt_report_t* report, double* dx, double* dy) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    upload_reduced(c, ht_val, j_val, r_x, r_y);
+    hykkt_report_t r{};
+    solve_resident(c, cfg ? *cfg : d, delta_min_inout, flags, &r);
+    if (r.status <= 1) download_solution(c, dx, nullptr, dy, nullptr);
+    if (report) *report = r;
+  });
+}
+
+int hykkt_upload_values_device(hykkt_t h, const hykkt_values_t* values) {
+  return guarded([&] { upload_values(ctx(h), values, true); });
+}
+
+int hykkt_batch_upload_device(hykkt_t h, int64_t batch, const hykkt_values_t* values) {
+  return guarded([&] { batch_upload(ctx(h), batch, values, true); });
+}
+
+int hykkt_solution_device(hykkt_t h, const double** dx, const double** ds, const double** dy,
+                          const double** dyd) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_kkt) throw StateError("no analysis");
+    if (dx) *dx = c.o.dx;
+    if (ds) *ds = c.o.ds;
+    if (dy) *dy = c.o.dy;
+    if (dyd) *dyd = c.o.dyd;
+  });
+}
+
+int hykkt_batch_solution_device(hykkt_t h, const double** dx, const double** ds, const double** dy,
+                                const double** dyd) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (c.batch <= 0) throw StateError("no batch uploaded");
+    const KktPlan& k = c.kp;
+    const idx B = c.batch;
+    const double* o = c.bouts.p;
+    if (dx) *dx = o;
+    if (dy) *dy = o + B * k.nx;
+    if (ds) *ds = o + B * (k.nx + k.mc);
+    if (dyd) *dyd = o + B * (k.nx + k.mc + k.md);
+  });
+}
+
+int hykkt_assemble(hykkt_t h, const hykkt_config_t* cfg, double* hg_val, double* r_hat_x) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_kkt) throw StateError("hykkt_analyze / hykkt_analyze_reduced must be called first");
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    const hykkt_config_t& cf = cfg ? *cfg : d;
+    validate_cfg(cf);
+    assemble_phase(c, cf);
+    if (hg_val && c.kp.hg.nnz())
+      CK(cudaMemcpyAsync(hg_val, c.hg.p, c.kp.hg.nnz() * sizeof(double), cudaMemcpyDefault, c.stream));
+    if (r_hat_x && c.kp.nx)
+      CK(cudaMemcpyAsync(r_hat_x, c.rhat.p, c.kp.nx * sizeof(double), cudaMemcpyDefault, c.stream));
+    read_status(c);
+  });
+}
+
+int hykkt_hgamma_pattern(hykkt_t h, int64_t* colptr, int64_t* rowidx) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_kkt) throw StateError("no KKT analysis");
+    if (colptr) std::copy(c.kp.hg.cp.begin(), c.kp.hg.cp.end(), colptr);
+    if (rowidx) std::copy(c.kp.hg.ri.begin(), c.kp.hg.ri.end(), rowidx);
+  });
+}
+
+int hykkt_factor_ladder(hykkt_t h, const hykkt_config_t* cfg, const double* values, double* delta_min_inout,
+                        int64_t* attempts, double* delta1, int64_t* failed_column) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_plan) throw StateError("no analysis");
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    const hykkt_config_t& cf = cfg ? *cfg : d;
+    validate_cfg(cf);
+    LadderOut lo;
+    if (c.have_kkt) {
+      if (values) throw InvalidArgument("KKT handle: the ladder runs on the assembled H_gamma (values must be NULL)");
+      if (!c.have_assembled) throw StateError("hykkt_assemble must be called first");
+      lo = ladder_phase(c, cf, c.hg.p, c.maxdiag.p, delta_min_inout);
+    } else {
+      const idx nnz = static_cast<idx>(c.sp.src_to_panel.size());
+      if (c.src_vals.n < static_cast<std::size_t>(std::max<idx>(nnz, 1))) c.src_vals.alloc(std::max<idx>(nnz, 1));
+      copy_in(c.src_vals.p, values, nnz, "values", c.stream, false);
+      c.maxdiag.alloc(1);
+      CK(cudaMemsetAsync(c.maxdiag.p, 0, sizeof(double), c.stream));
+      if (nnz > 0) {
+        dev::k_maxdiag_src<<<blocks_for(nnz), kThreads, 0, c.stream>>>(static_cast<int>(nnz), c.src_vals.p,
+                                                                       c.src_row.p, c.src_col.p, c.maxdiag.p);
+        check_launch(c);
+      }
+      lo = ladder_phase(c, cf, c.src_vals.p, c.maxdiag.p, delta_min_inout);
+    }
+    if (attempts) *attempts = lo.attempts;
+    if (delta1) *delta1 = lo.delta1;
+    if (failed_column) *failed_column = lo.failed;
+  });
+}
+
+int hykkt_chol_set_factor(hykkt_t h, const double* l_values) {
+  return guarded([&] { set_factor(ctx(h), l_values); });
+}
+
+int hykkt_chol_set_j(hykkt_t h, int64_t m_c, const int64_t* j_colptr, const int64_t* j_rowidx,
+                     const double* j_val) {
+  return guarded([&] { chol_set_j(ctx(h), m_c, j_colptr, j_rowidx, j_val); });
+}
+
+int hykkt_cg_schur(hykkt_t h, const hykkt_config_t* cfg, const double* rhs, double delta2, double* x,
+                   int64_t* iterations, double* relative_residual, int32_t* converged,
+                   int32_t* small_quadratic) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    require_factor(c);
+    if (!c.have_j) throw StateError("no constraint Jacobian on this handle (hykkt_chol_set_j)");
+    hykkt_config_t d;
+    hykkt_config_default(&d);
+    const hykkt_config_t& cf = cfg ? *cfg : d;
+    validate_cfg(cf);
+    if (delta2 < 0.0) throw InvalidArgument("delta2 must be >= 0");
+    const idx mc = c.kp.mc;
+    dev::CgResultDev r{0, 0.0, 1, 0};
+    if (mc > 0) {
+      copy_in(c.cg_rhs.p, rhs, mc, "rhs", c.stream, false);
+      CK(cudaMemsetAsync(&c.status.p->abort, 0, sizeof(int), c.stream));
+      r = run_cg(c, cf, delta2);
+      if (x) CK(cudaMemcpyAsync(x, c.cg_x.p, mc * sizeof(double), cudaMemcpyDefault, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+    }
+    if (iterations) *iterations = r.iterations;
+    if (relative_residual) *relative_residual = r.relres;
+    if (converged) *converged = r.converged;
+    if (small_quadratic) *small_quadratic = r.small_quadratic;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Per-handle scheduling knobs (no effect on results): "ks_lpt" = 1 / 0 turns
+// the history longest-first system order of the batched solve on / off.
+int hykkt_set_option(hykkt_t h, const char* name, int64_t value) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!name) throw InvalidArgument("null option name");
+    const std::string n(name);
+    if (n == "ks_lpt") {
+      c.ks.lpt_on = value ? 1 : 0;
+    } else {
+      throw InvalidArgument("unknown option: " + n);
+    }
   });
 }
 

@@ -186,6 +186,20 @@ __global__ void k_scatter(int nsrc, const double* __restrict__ src,
   panel[src_to_panel[t]] = v;
 }
 
+// v[i] = value (identity Ruiz scaling of the Reduced2x2 entry points).
+__global__ void k_fill(double* __restrict__ v, int n, double value) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) v[t] = value;
+}
+
+// max |diag| of a matrix given as values in `src` CSC order
+// (max_abs_diagonal, solver.cpp:30-42) for the Cholesky-level ladder.
+__global__ void k_maxdiag_src(int nsrc, const double* __restrict__ src, const int* __restrict__ src_row,
+                              const int* __restrict__ src_col, double* __restrict__ maxdiag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nsrc && src_row[t] == src_col[t]) atomic_max_nonneg(maxdiag, fabs(src[t]));
+}
+
 // Unscale + recover (ruiz.cpp:118-133, kkt_system.cpp:89-105).
 __global__ void k_recover(AsmPlan p, const int* __restrict__ jd_rp,
                           const int* __restrict__ jd_ci,

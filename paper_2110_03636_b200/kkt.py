@@ -1,8 +1,10 @@
 """Host-side value types mirroring the reference's (plain numpy arrays).
 
 CscMatrix      <- hkkt::CscMatrix   (proj/core/include/hkkt/csc_matrix.hpp:41-94)
-BlockKkt4x4    <- hkkt::BlockKkt4x4 (proj/core/include/hkkt/kkt_system.hpp:274-296)
-FullSolution   <- hkkt::FullSolution (kkt_system.hpp:310-315)
+BlockKkt4x4    <- hkkt::BlockKkt4x4 (proj/core/include/hkkt/kkt_system.hpp:31-50)
+FullSolution   <- hkkt::FullSolution (kkt_system.hpp:66-71)
+Reduced2x2     <- hkkt::Reduced2x2 (kkt_system.hpp:56-64)
+HGammaSystem   <- hkkt::HGammaSystem (solver.hpp:69-73)
 
 Indices are int64 like the reference (csc_matrix.hpp:25); the device path
 narrows them to int32 at the C-ABI boundary.
@@ -118,3 +120,31 @@ class FullSolution:
 
     def stacked(self) -> np.ndarray:
         return np.concatenate([self.dx, self.ds, self.dy, self.dyd])
+
+
+@dataclass
+class Reduced2x2:
+    """[[H_tilde, J^T], [J, 0]] with right-hand side (r_x, r_y); H_tilde
+    lower triangle with its full diagonal."""
+    h_tilde: CscMatrix
+    j: CscMatrix
+    r_x: np.ndarray
+    r_y: np.ndarray
+
+    @property
+    def n_x(self) -> int:
+        return self.h_tilde.ncols
+
+    @property
+    def m_c(self) -> int:
+        return self.j.nrows
+
+    def same_pattern_as(self, o: "Reduced2x2") -> bool:
+        return self.h_tilde.same_pattern_as(o.h_tilde) and self.j.same_pattern_as(o.j)
+
+
+@dataclass
+class HGammaSystem:
+    h_gamma: CscMatrix  # lower triangle
+    r_hat_x: np.ndarray
+    gamma_used: float = 0.0

@@ -5,6 +5,9 @@ Names, argument meaning, defaults and outcomes follow
 
   SolverConfig / RegularizationState / SolveStatus / SolveReport   solver.hpp:29-150
   solve_full / solve_sequence / SequenceResult                     solver.hpp:172-205
+  solve_reduced / ReducedSolveResult                               solver.hpp:152-170
+  assemble_h_gamma / factorize_with_ladder / LadderFailure          solver.hpp:75-94
+  cg_schur / CgResult                                              solver.hpp:110-122
   symbolic_cholesky / numeric_cholesky / factor_solve              cholesky.hpp:41-83
   NotSpdFailure                                                    cholesky.hpp:47-50
 
@@ -23,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, dp, f64, i64, ip
-from .kkt import BlockKkt4x4, CscMatrix, FullSolution
+from .kkt import BlockKkt4x4, CscMatrix, FullSolution, HGammaSystem, Reduced2x2
 
 
 @dataclass
@@ -136,6 +139,33 @@ class NotSpdFailure:
     pivot: float
 
 
+@dataclass
+class LadderFailure:
+    attempts: int
+    last_delta1: float
+    failed_column: int
+
+
+@dataclass
+class CgResult:
+    x: np.ndarray
+    iterations: int = 0
+    relative_residual: float = 0.0
+    converged: bool = False
+    small_quadratic_detected: bool = False
+
+
+@dataclass
+class ReducedSolveResult:
+    dx: Optional[np.ndarray]
+    dy: Optional[np.ndarray]
+    report: SolveReport
+    symbolic_created: bool = False
+
+    def ok(self) -> bool:
+        return is_success(self.report.status)
+
+
 def check_dims(sys: BlockKkt4x4) -> None:
     """BlockKkt4x4::validate (kkt_system.cpp:33-54), dimension part."""
     nx, mc, md = sys.n_x, sys.m_c, sys.m_d
@@ -204,6 +234,74 @@ class Device:
         check(_lib.lib().hykkt_get_perm(self.h, ip(out)))
         return out
 
+    def analyze_reduced(self, red: Reduced2x2, perm=None) -> None:
+        """Per-pattern half of solve_reduced (solver.cpp:230-235) for a
+        Reduced2x2 caller."""
+        L = _lib.lib()
+        a = [i64(x) for x in (red.h_tilde.colptr, red.h_tilde.rowidx, red.j.colptr, red.j.rowidx)]
+        p = None if perm is None else i64(perm)
+        check(L.hykkt_analyze_reduced(self.h, red.n_x, red.m_c, *[ip(x) for x in a], ip(p)))
+        self._pattern = red
+
+    def solve_reduced(self, red: Reduced2x2, cfg: SolverConfig | None = None,
+                      state: RegularizationState | None = None,
+                      metrics: bool = True) -> ReducedSolveResult:
+        """hkkt::solve_reduced (solver.cpp:222-293): assemble H_gamma, ladder,
+        w solve, CG with the delta2 restart, dx solve; no Ruiz, no recovery."""
+        cfg = cfg or SolverConfig()
+        created = False
+        if not isinstance(self._pattern, Reduced2x2) or not self._pattern.same_pattern_as(red):
+            self.analyze_reduced(red)
+            created = True
+        if state is None:
+            state = RegularizationState.initial(cfg)
+        arrs = [f64(x) for x in (red.h_tilde.values, red.j.values, red.r_x, red.r_y)]
+        dx, dy = np.zeros(red.n_x), np.zeros(red.m_c)
+        rep = _lib.Report()
+        dm = C.c_double(state.delta_min_current)
+        check(_lib.lib().hykkt_solve_reduced(self.h, C.byref(cfg.c()), *[dp(a) for a in arrs], C.byref(dm),
+                                             _lib.FLAG_METRICS if metrics else 0, C.byref(rep), dp(dx),
+                                             dp(dy)))
+        state.delta_min_current = dm.value
+        state.delta1 = rep.delta1_final
+        state.attempts = rep.factorization_attempts
+        report = SolveReport.from_c(rep)
+        ok = is_success(report.status)
+        return ReducedSolveResult(dx if ok else None, dy if ok else None, report, created)
+
+    def assemble(self, cfg: SolverConfig | None = None) -> HGammaSystem:
+        """assemble_h_gamma (solver.cpp:66-84) on the uploaded values (a
+        reduced handle: the Reduced2x2 as given; a block-4x4 handle: the
+        Ruiz-scaled reduction of the system)."""
+        cfg = cfg or SolverConfig()
+        info = self.info()
+        n, nnz = info["n"], info["nnz_h_gamma"]
+        cp, ri = np.zeros(n + 1, np.int64), np.zeros(nnz, np.int64)
+        vals, rhat = np.zeros(nnz), np.zeros(n)
+        L = _lib.lib()
+        check(L.hykkt_assemble(self.h, C.byref(cfg.c()), dp(vals), dp(rhat)))
+        check(L.hykkt_hgamma_pattern(self.h, ip(cp), ip(ri)))
+        return HGammaSystem(CscMatrix(n, n, cp, ri, vals), rhat, cfg.gamma)
+
+    def factorize_with_ladder(self, cfg: SolverConfig, state: RegularizationState):
+        """factorize_with_ladder (solver.cpp:108-142) on the H_gamma of the
+        last assemble(); returns None on success or a LadderFailure."""
+        return _ladder(self.h, cfg, None, state)
+
+    def upload_reduced(self, red: Reduced2x2) -> None:
+        arrs = [f64(x) for x in (red.h_tilde.values, red.j.values, red.r_x, red.r_y)]
+        self._keep = arrs
+        check(_lib.lib().hykkt_upload_reduced(self.h, *[dp(a) for a in arrs]))
+
+    def cg_schur(self, rhs, cfg: SolverConfig | None = None, delta2: float = 0.0) -> CgResult:
+        return _cg_schur(self.h, rhs, cfg or SolverConfig(), delta2)
+
+    def factor_solve(self, b) -> np.ndarray:
+        b = f64(b)
+        x = np.zeros(b.shape[0])
+        check(_lib.lib().hykkt_chol_solve(self.h, dp(b), dp(x)))
+        return x
+
     # ---- values ------------------------------------------------------------
     def _values(self, sys: BlockKkt4x4):
         arrs = [f64(x) for x in (sys.h.values, sys.j.values, sys.j_d.values, sys.d_x, sys.d_s,
@@ -235,6 +333,10 @@ class Device:
                                                  dp(out.dyd)))
         return out
 
+    def set_option(self, name: str, value: int) -> None:
+        """Scheduling knobs (hykkt_set_option), e.g. ("ks_lpt", 0)."""
+        check(_lib.lib().hykkt_set_option(self.h, name.encode(), int(value)))
+
     def timing(self) -> dict:
         t = _lib.Timing()
         check(_lib.lib().hykkt_last_timing(self.h, C.byref(t)))
@@ -248,7 +350,7 @@ class Device:
         cfg = cfg or SolverConfig()
         check_dims(sys)
         created = False
-        if self._pattern is None or not self._pattern.same_pattern_as(sys):
+        if not isinstance(self._pattern, BlockKkt4x4) or not self._pattern.same_pattern_as(sys):
             self.analyze(sys)
             created = True
         if state is None:
@@ -275,11 +377,34 @@ def solve_full(sys: BlockKkt4x4, cfg: SolverConfig | None = None, shared: Device
     return dev.solve_full(sys, cfg, state)
 
 
+def _ladder(h, cfg: SolverConfig, values, state: RegularizationState):
+    dm = C.c_double(state.delta_min_current)
+    att, d1, fc = C.c_int64(0), C.c_double(0.0), C.c_int64(-1)
+    v = None if values is None else f64(values)
+    check(_lib.lib().hykkt_factor_ladder(h, C.byref(cfg.c()), dp(v), C.byref(dm), C.byref(att),
+                                         C.byref(d1), C.byref(fc)))
+    state.delta_min_current = dm.value
+    state.delta1 = d1.value
+    state.attempts = att.value
+    return None if fc.value < 0 else LadderFailure(att.value, d1.value, fc.value)
+
+
+def _cg_schur(h, rhs, cfg: SolverConfig, delta2: float) -> CgResult:
+    rhs = f64(rhs)
+    x = np.zeros(rhs.shape[0])
+    it, rr = C.c_int64(0), C.c_double(0.0)
+    conv, sq = C.c_int32(0), C.c_int32(0)
+    check(_lib.lib().hykkt_cg_schur(h, C.byref(cfg.c()), dp(rhs), delta2, dp(x), C.byref(it),
+                                    C.byref(rr), C.byref(conv), C.byref(sq)))
+    return CgResult(x, it.value, rr.value, bool(conv.value), bool(sq.value))
+
+
 def solve_sequence(systems: Sequence[BlockKkt4x4], cfg: SolverConfig | None = None,
-                   device: int = 0) -> SequenceResult:
+                   device: int = 0, perm=None) -> SequenceResult:
     """hkkt::solve_sequence (solver.cpp:352-412): one symbolic analysis when
     the patterns are uniform, delta_min carried across, failures recorded
-    and the sequence continued."""
+    and the sequence continued.  `perm` (optional) is the ordering of the
+    shared symbolic analysis (the reference computes amd_order there)."""
     if len(systems) == 0:
         raise _lib.InvalidMatrixError(-1, "solve_sequence: empty sequence")
     cfg = cfg or SolverConfig()
@@ -290,6 +415,9 @@ def solve_sequence(systems: Sequence[BlockKkt4x4], cfg: SolverConfig | None = No
     for k, sys in enumerate(systems):
         if not res.pattern_uniform:
             dev._pattern = None
+        if dev._pattern is None and perm is not None and (res.pattern_uniform or k == 0):
+            dev.analyze(sys, perm)
+            res.stats.symbolic_analyses += 1
         r = dev.solve_full(sys, cfg, state)
         r.report.symbolic_reused = res.pattern_uniform and k > 0
         if r.symbolic_created:
@@ -333,6 +461,30 @@ class CholeskyFactor:
         x = np.zeros(self.n)
         check(_lib.lib().hykkt_chol_solve(self.dev.h, dp(b), dp(x)))
         return x
+
+    def factorize_with_ladder(self, values, cfg: SolverConfig, state: RegularizationState):
+        """factorize_with_ladder (solver.cpp:108-142) on a matrix in this
+        factor's pattern (an HGammaSystem's h_gamma values); None on
+        success or a LadderFailure."""
+        r = _ladder(self.dev.h, cfg, values, state)
+        self.ok = r is None
+        return r
+
+    def set_factor(self, l_values) -> None:
+        """Load reference-layout L values (NumericCholesky::l_values)."""
+        v = f64(l_values)
+        check(_lib.lib().hykkt_chol_set_factor(self.dev.h, dp(v)))
+        self.ok = True
+
+    def set_j(self, j: CscMatrix) -> None:
+        """The J of SchurOperator (solver.hpp:97-103) for cg_schur."""
+        self._j = [i64(j.colptr), i64(j.rowidx), f64(j.values)]
+        check(_lib.lib().hykkt_chol_set_j(self.dev.h, j.nrows, ip(self._j[0]), ip(self._j[1]),
+                                          dp(self._j[2])))
+
+    def cg_schur(self, rhs, cfg: SolverConfig | None = None, delta2: float = 0.0) -> CgResult:
+        """cg_schur (solver.cpp:154-201) on S = J H^-1 J^T + delta2 I."""
+        return _cg_schur(self.dev.h, rhs, cfg or SolverConfig(), delta2)
 
     def factor(self) -> dict:
         info = self.dev.info()
@@ -415,6 +567,14 @@ class Batch:
         self._keep = arrs
         v = _lib.Values(*[dp(a) for a in arrs])
         check(_lib.lib().hykkt_batch_upload(self.dev.h, self.count, C.byref(v)))
+
+    def upload_device(self, ptrs: dict, count: int) -> None:
+        """Values already in device memory (hykkt_batch_upload_device):
+        `ptrs` maps each VALUE_FIELDS name to a device address of a
+        [system][entry] float64 array; copied device-to-device."""
+        self.count = int(count)
+        v = _lib.Values(*[C.cast(C.c_void_p(int(ptrs[n])), _lib.F64P) for n in VALUE_FIELDS])
+        check(_lib.lib().hykkt_batch_upload_device(self.dev.h, self.count, C.byref(v)))
 
     def solve_resident(self, cfg: SolverConfig, metrics: bool = False, timing: bool = False):
         reps = (_lib.Report * self.count)()
