@@ -103,6 +103,7 @@ typedef struct {
   int64_t panel_slots;    /* dense supernodal storage, doubles */
   double factor_flops;    /* sum_j c_j^2 */
   int64_t nnz_j, nnz_jd, m_c, m_d;
+  int64_t explicit_zeros; /* panel entries outside L's pattern (relaxed amalgamation) */
 } hykkt_analysis_t;
 
 /* Device-side phase timings of the last solve, milliseconds (CUDA events on
@@ -282,9 +283,13 @@ int hykkt_cg_schur(hykkt_t h, const hykkt_config_t* cfg, const double* rhs,
                    double* relative_residual, int32_t* converged,
                    int32_t* small_quadratic);
 
-/* Scheduling knobs of a handle (never change results): "ks_lpt" = 1 (default)
- * / 0 — the batched solve takes systems longest-first by the previous call's
- * CG iteration counts / in natural order. */
+/* Knobs of a handle: "ks_lpt" = 1 (default) / 0 — the batched solve takes
+ * systems longest-first by the previous call's CG iteration counts / in
+ * natural order (never changes results); "amalg_width" (columns) and
+ * "amalg_zeros_pct" — relaxed amalgamation of elimination-tree chains into
+ * supernodes of at most that width and share of explicit zeros, applied by
+ * the next hykkt_analyze / hykkt_chol_analyze (amalg_width <= 1: fundamental
+ * supernodes only; changes only rounding). */
 int hykkt_set_option(hykkt_t h, const char* name, int64_t value);
 
 #ifdef __cplusplus

@@ -64,6 +64,7 @@ class Analysis(C.Structure):
         ("etree_height", C.c_int64), ("max_sn_width", C.c_int64), ("max_sn_rows", C.c_int64),
         ("panel_slots", C.c_int64), ("factor_flops", C.c_double),
         ("nnz_j", C.c_int64), ("nnz_jd", C.c_int64), ("m_c", C.c_int64), ("m_d", C.c_int64),
+        ("explicit_zeros", C.c_int64),
     ]
 
 

@@ -2,6 +2,7 @@
 #include "analyze.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <queue>
 #include <utility>
@@ -174,8 +175,17 @@ std::vector<idx> minimum_degree_order(const CscPattern& lower) {
   return perm;
 }
 
+AmalgParams AmalgParams::defaults() {
+  AmalgParams p{1, 0.6};
+  if (const char* e = std::getenv("HYKKT_AMALG_W")) p.width = std::atoi(e);
+  if (const char* e = std::getenv("HYKKT_AMALG_Z")) p.zeros = std::atof(e);
+  return p;
+}
+
 SupernodalPlan build_supernodal_plan(const CscPattern& a,
-                                     std::vector<idx> perm) {
+                                     std::vector<idx> perm, AmalgParams amalg) {
+  const idx amalg_width = amalg.width;
+  const double amalg_zeros = amalg.zeros;
   a.validate("pattern");
   if (a.nrows != a.ncols) fail("symbolic analysis requires a square pattern");
   const idx n = a.ncols;
@@ -229,19 +239,43 @@ SupernodalPlan build_supernodal_plan(const CscPattern& a,
     }
   }
 
-  // Fundamental supernodes: j joins j-1's supernode when j is j-1's parent,
-  // its only child, and the column structures nest exactly.
+  // Supernodes.  Column j joins the supernode of j-1 when j is j-1's parent
+  // and its only child (a chain in the elimination tree) and either
+  //   * the column structures nest exactly (fundamental supernodes), or
+  //   * relaxed amalgamation: the merged supernode stays at most
+  //     `amalg_width` columns wide and at most `amalg_zeros` of its panel
+  //     entries are explicit zeros.
+  // Along such a chain every column's structure below the supernode lies in
+  // the last column's, so the merged row structure is the own columns plus
+  // the last column's rows below it.  Explicit zeros stay exactly zero
+  // through the factorization (their updates are products with structural
+  // zeros), so results are unchanged; what changes is that a chain of
+  // narrow supernodes — one cross-SM hand-off per link in the sync-free
+  // solves — becomes one dense diagonal block solved inside one warp/CTA.
   std::vector<idx> nchild(n, 0);
   for (idx j = 0; j < n; ++j) {
     if (s.parent[j] >= 0) nchild[s.parent[j]]++;
   }
   s.sn_of.assign(n, 0);
   s.sn_first.clear();
-  for (idx j = 0; j < n; ++j) {
-    const bool merge = j > 0 && s.parent[j - 1] == j && nchild[j] == 1 &&
-                       s.col_counts[j - 1] == s.col_counts[j] + 1;
-    if (!merge) s.sn_first.push_back(static_cast<int>(j));
-    s.sn_of[j] = static_cast<int>(s.sn_first.size()) - 1;
+  {
+    idx f = 0, truth = 0;  // current supernode's first column and true L entries
+    for (idx j = 0; j < n; ++j) {
+      bool merge = j > 0 && s.parent[j - 1] == j && nchild[j] == 1;
+      if (merge && s.col_counts[j - 1] != s.col_counts[j] + 1) {
+        const idx w = j - f + 1, nr = w + s.col_counts[j] - 1;
+        const idx entries = w * nr - w * (w - 1) / 2;
+        const idx zeros = entries - (truth + s.col_counts[j]);
+        merge = w <= amalg_width && static_cast<double>(zeros) <= amalg_zeros * static_cast<double>(entries);
+      }
+      if (!merge) {
+        s.sn_first.push_back(static_cast<int>(j));
+        f = j;
+        truth = 0;
+      }
+      truth += s.col_counts[j];
+      s.sn_of[j] = static_cast<int>(s.sn_first.size()) - 1;
+    }
   }
   s.nsup = static_cast<idx>(s.sn_first.size());
   s.sn_first.push_back(static_cast<int>(n));
@@ -251,20 +285,23 @@ SupernodalPlan build_supernodal_plan(const CscPattern& a,
   s.sn_off.assign(ns + 1, 0);
   s.sn_rows_ptr.assign(ns + 1, 0);
   for (idx k = 0; k < ns; ++k) {
-    const idx f = s.sn_first[k], w = s.sn_first[k + 1] - f;
-    s.sn_nrows[k] = static_cast<int>(s.col_counts[f]);
+    const idx f = s.sn_first[k], w = s.sn_first[k + 1] - f, last = f + w - 1;
+    s.sn_nrows[k] = static_cast<int>(w + s.col_counts[last] - 1);
     s.sn_off[k + 1] = s.sn_off[k] + idx{s.sn_nrows[k]} * w;
     s.sn_rows_ptr[k + 1] = s.sn_rows_ptr[k] + s.sn_nrows[k];
     s.max_width = std::max<int>(s.max_width, static_cast<int>(w));
     s.max_nrows = std::max(s.max_nrows, s.sn_nrows[k]);
+    s.explicit_zeros += idx{s.sn_nrows[k]} * w - w * (w - 1) / 2;
   }
+  s.explicit_zeros -= s.l_cp[n];
   s.panel_size = s.sn_off[ns];
   if (s.panel_size >= (idx{1} << 31)) fail("supernodal panels exceed 2^31 slots");
   s.sn_rows.resize(s.sn_rows_ptr[ns]);
   for (idx k = 0; k < ns; ++k) {
-    const idx f = s.sn_first[k];
-    std::copy(s.l_ri.begin() + s.l_cp[f], s.l_ri.begin() + s.l_cp[f + 1],
-              s.sn_rows.begin() + s.sn_rows_ptr[k]);
+    const idx f = s.sn_first[k], w = s.sn_first[k + 1] - f, last = f + w - 1;
+    int* out = s.sn_rows.data() + s.sn_rows_ptr[k];
+    for (idx c = 0; c < w; ++c) out[c] = static_cast<int>(f + c);
+    std::copy(s.l_ri.begin() + s.l_cp[last] + 1, s.l_ri.begin() + s.l_cp[last + 1], out + w);
   }
 
   // Supernode tree, levels, children, level-sorted order.
@@ -414,12 +451,24 @@ SupernodalPlan build_supernodal_plan(const CscPattern& a,
   s.diag_panel.resize(n);
   for (idx j = 0; j < n; ++j) {
     const int k = s.sn_of[j];
-    const int f = s.sn_first[k], nr = s.sn_nrows[k];
+    const int f = s.sn_first[k], w = s.sn_first[k + 1] - f, nr = s.sn_nrows[k];
     const idx c = j - f;
-    const idx base = s.sn_off[k] + c * nr + c;
-    s.diag_panel[j] = static_cast<int>(base);
+    const idx col0 = s.sn_off[k] + c * nr;
+    s.diag_panel[j] = static_cast<int>(col0 + c);
+    // rows of column j inside the supernode's (possibly amalgamated) structure
+    const int* rows = s.sn_rows.data() + s.sn_rows_ptr[k];
+    const int* lo = rows + w;
     for (idx t = 0; t < s.col_counts[j]; ++t) {
-      s.l_to_panel[s.l_cp[j] + t] = static_cast<int>(base + t);
+      const idx r = s.l_ri[s.l_cp[j] + t];
+      idx pos;
+      if (r < f + w) {
+        pos = r - f;
+      } else {
+        lo = std::lower_bound(lo, rows + nr, static_cast<int>(r));
+        if (lo == rows + nr || *lo != r) fail("internal: L entry outside its supernode structure");
+        pos = lo - rows;
+      }
+      s.l_to_panel[s.l_cp[j] + t] = static_cast<int>(col0 + pos);
     }
   }
 

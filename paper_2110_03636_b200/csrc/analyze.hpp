@@ -99,12 +99,24 @@ struct SupernodalPlan {
   idx l_nnz() const { return l_cp.empty() ? 0 : l_cp.back(); }
   double factor_flops = 0.0;  // sum_j c_j^2 (CSparse convention)
   int max_width = 0, max_nrows = 0;
+  idx explicit_zeros = 0;     // panel entries outside L's pattern (amalgamation)
+};
+
+// Relaxed amalgamation of elimination-tree chains (build_supernodal_plan):
+// merged supernodes at most `width` columns wide with at most `zeros` of
+// their panel entries explicit zeros.  width <= 1 keeps fundamental
+// supernodes only.  Defaults: HYKKT_AMALG_W / HYKKT_AMALG_Z or the B200 sweep.
+struct AmalgParams {
+  int width;
+  double zeros;
+  static AmalgParams defaults();
 };
 
 // Builds the plan for the lower-triangle pattern `a` (n x n, original
 // indices) under `perm` (empty => own minimum-degree ordering).
 SupernodalPlan build_supernodal_plan(const CscPattern& a,
-                                     std::vector<idx> perm);
+                                     std::vector<idx> perm,
+                                     AmalgParams amalg = AmalgParams::defaults());
 
 // Own fill-reducing ordering: minimum degree on the explicit elimination
 // graph, lowest index first on ties, followed by an etree postorder.

@@ -30,6 +30,7 @@
 #include "kernels_batch.cuh"
 #include "kernels_sys.cuh"
 #include "kernels_mf.cuh"
+#include "kernels_metrics.cuh"
 #include "sysplan.hpp"
 
 namespace hykkt {
@@ -124,9 +125,11 @@ struct hykkt_context {
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
   bool ruiz_rows_built = false;
+  hykkt::DBuf<double> met_partials;  // device BE / RR (kernels_metrics.cuh)
 
   bool have_plan = false, have_kkt = false, have_values = false, have_factor = false;
   bool have_assembled = false;
+  hykkt::AmalgParams amalg = hykkt::AmalgParams::defaults();  // hykkt_set_option, before analysis
   // Reduced2x2 handle (hykkt_analyze_reduced): m_d = 0, D_x = 0 and identity
   // Ruiz scaling, so the 4x4 kernels compute solve_reduced exactly
   bool reduced = false;
@@ -734,7 +737,7 @@ void analyze_kkt(Ctx& c, idx nx, idx mc, idx md, const std::int64_t* hcp, const 
   c.kp = build_kkt_plan(nx, mc, md, h, j, jd);
   std::vector<idx> pv;
   if (perm) pv.assign(perm, perm + nx);
-  c.sp = build_supernodal_plan(c.kp.hg, std::move(pv));
+  c.sp = build_supernodal_plan(c.kp.hg, std::move(pv), c.amalg);
   upload_plan(c, c.kp.hg);
   const KktPlan& k = c.kp;
   cudaStream_t st = c.stream;
@@ -1105,9 +1108,74 @@ void solve_resident(Ctx& c, const hykkt_config_t& cfg, double* dmin_inout, int f
   if (rep) *rep = r;
 }
 
-// BE / RR of the 2x2 scaled, 2x2 and 4x4 systems (metrics.cpp:28-240) on
-// the host from the downloaded solution (outside the device path).
+void ruiz_rows_prepare(Ctx& c);
+
+// BE / RR of the 4x4, 2x2 and scaled 2x2 systems (metrics.cpp:28-240) on
+// the device (kernels_metrics.cuh): only the six numbers come back.
+// HYKKT_METRICS_HOST=1 computes them on the host from downloaded vectors
+// instead (the cross-check of tests/test_gpu_api.py).
+void metrics_host(Ctx& c, hykkt_report_t& r);
 void metrics_phase(Ctx& c, hykkt_report_t& r) {
+  const bool host = std::getenv("HYKKT_METRICS_HOST") && std::atoi(std::getenv("HYKKT_METRICS_HOST")) != 0;
+  if (host) {
+    metrics_host(c, r);
+    return;
+  }
+  const KktPlan& k = c.kp;
+  ruiz_rows_prepare(c);
+  dev::MetricsArgs ma;
+  ma.p = c.asmplan();
+  ma.rows_ptr = c.ruiz_rp.p;
+  ma.rows_ent = reinterpret_cast<const int4*>(c.ruiz_ent.p);
+  ma.jd_rp = c.jdcsr_rp.p;
+  ma.jd_ci = c.jdcsr_ci.p;
+  ma.jd_src = c.jdcsr_src.p;
+  ma.h = c.v.h;
+  ma.j = c.v.j;
+  ma.jd = c.v.jd;
+  ma.d_x = c.v.dx;
+  ma.d_s = c.v.ds;
+  ma.r_tx = c.v.rtx;
+  ma.r_s = c.v.rs;
+  ma.r_y = c.v.ry;
+  ma.r_yd = c.v.ryd;
+  ma.dx = c.o.dx;
+  ma.ds = c.o.ds;
+  ma.dy = c.o.dy;
+  ma.dyd = c.o.dyd;
+  ma.ht = c.ht.p;
+  ma.rx = c.r_x.p;
+  ma.hts = c.hts.p;
+  ma.js = c.js.p;
+  ma.rxs = c.rxs.p;
+  ma.rys = c.rys.p;
+  ma.dx_s = c.dx_s.p;
+  ma.dy_s = c.cg_x.p;
+  ma.with_4x4 = c.reduced ? 0 : 1;
+  const long long rows = std::max<long long>(k.nx + k.mc, k.nx + 2 * k.md + k.mc);
+  const int grid = std::max(1, std::min(blocks_for(rows), 2 * c.num_sms));
+  c.met_partials.alloc(static_cast<std::size_t>(grid) * dev::kMetSlots + 6);
+  ma.partials = c.met_partials.p;
+  double* out = c.met_partials.p + static_cast<std::size_t>(grid) * dev::kMetSlots;
+  dev::k_metrics_rows<<<grid, kThreads, 0, c.stream>>>(ma);
+  check_launch(c);
+  dev::k_metrics_final<<<1, kThreads, 0, c.stream>>>(c.met_partials.p, grid, out);
+  check_launch(c);
+  double v[6];
+  CK(cudaMemcpyAsync(v, out, sizeof(v), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  if (!c.reduced) {
+    r.be_4x4 = v[0];
+    r.rr_4x4 = v[1];
+  }
+  r.be_2x2 = v[2];
+  r.rr_2x2 = v[3];
+  r.be_2x2_scaled = v[4];
+  r.rr_2x2_scaled = v[5];
+}
+
+// Host form of the same reports (downloads every vector; diagnostics).
+void metrics_host(Ctx& c, hykkt_report_t& r) {
   const KktPlan& k = c.kp;
   const idx nx = k.nx, mc = k.mc, md = k.md;
   auto dl = [&](const double* src, idx n) {
@@ -2162,6 +2230,7 @@ static hykkt_analysis_t stats_of(const SupernodalPlan& s, const KktPlan* kp) {
     a.nnz_jd = kp ? kp->jd.nnz() : 0;
     a.m_c = kp ? kp->mc : 0;
     a.m_d = kp ? kp->md : 0;
+    a.explicit_zeros = s.explicit_zeros;
     return a;
 }
 
@@ -2374,7 +2443,7 @@ int hykkt_chol_analyze(hykkt_t h, int64_t n, const int64_t* colptr, const int64_
     c.have_j = false;
     c.kp = KktPlan{};
     c.kp.hg = a;  // source pattern for scatter bookkeeping
-    c.sp = build_supernodal_plan(a, std::move(pv));
+    c.sp = build_supernodal_plan(a, std::move(pv), c.amalg);
     upload_plan(c, a);
     c.src_vals.alloc(a.nnz());
     CK(cudaStreamSynchronize(c.stream));
@@ -2820,6 +2889,11 @@ int hykkt_set_option(hykkt_t h, const char* name, int64_t value) {
     const std::string n(name);
     if (n == "ks_lpt") {
       c.ks.lpt_on = value ? 1 : 0;
+    } else if (n == "amalg_width") {
+      c.amalg.width = static_cast<int>(value);
+    } else if (n == "amalg_zeros_pct") {
+      if (value < 0 || value > 100) throw InvalidArgument("amalg_zeros_pct must be in [0, 100]");
+      c.amalg.zeros = static_cast<double>(value) / 100.0;
     } else {
       throw InvalidArgument("unknown option: " + n);
     }

@@ -320,3 +320,39 @@ def test_reanalysis_between_batched_solves(ref):
             assert rel(got, want.stacked()) <= 1e-8
             assert abs(reps[k].cg_iterations - want.report["cg_iterations"]) <= 1
     dev.close()
+
+
+# ---- device BE / RR (metrics.cpp:28-240 on the device) ----------------------------
+@pytest.mark.parametrize("nb,gamma", [(120, 1e4), (500, 1e8)])
+def test_device_metrics_match_host_and_reference(ref, nb, gamma, monkeypatch):
+    s = acopf.generate(nb, 7, 7)
+    cfg = SolverConfig(gamma=gamma)
+    perm = ref.hgamma_amd(s, cfg)
+    want = ref.solve_full(s, cfg, perm).report
+    dev = Device(0)
+    dev.analyze(s, perm)
+    d = dev.solve_full(s, cfg).report
+    monkeypatch.setenv("HYKKT_METRICS_HOST", "1")
+    h = dev.solve_full(s, cfg).report
+    for name in ("be_4x4", "rr_4x4", "be_2x2", "rr_2x2", "be_2x2_scaled", "rr_2x2_scaled"):
+        dv, hv, rv = getattr(d, name), getattr(h, name), want[name]
+        assert np.isfinite(dv), name
+        # rounding-level quantities: agree in magnitude, not digits
+        assert dv <= 10 * max(hv, 1e-17) and hv <= 10 * max(dv, 1e-17), (name, dv, hv)
+        assert dv <= 10 * max(rv, 1e-16), (name, dv, rv)
+    assert d.be_4x4 <= 1e-10
+    dev.close()
+
+
+def test_device_metrics_reduced_handle(ref):
+    s = ref.generate(60, 15, 12, seed=31)[0]
+    red = ref.reduce(s)
+    cfg = SolverConfig()
+    perm = ref.hgamma_amd(s, cfg)
+    want = ref.solve_reduced(red, cfg, perm)["report"]
+    dev = Device(0)
+    dev.analyze_reduced(red, perm)
+    r = dev.solve_reduced(red, cfg)
+    assert r.report.be_2x2 <= 10 * max(want["be_2x2"], 1e-16)
+    assert np.isnan(r.report.be_4x4)
+    dev.close()

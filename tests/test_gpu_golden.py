@@ -50,13 +50,23 @@ def test_single_system_matches_golden(name):
     dev.close()
 
 
-@pytest.mark.parametrize("path", ["default", "lane"])
+BATCH_PATHS = {
+    "default": {},
+    "lane": {"HYKKT_BATCH_PATH": "lane"},
+    # opt-in system-per-CTA factorization (kernels_sys.cuh ks_factor)
+    "ks_factor": {"HYKKT_KS_FACTOR": "1"},
+    "amalgamated": {"HYKKT_AMALG_W": "16", "HYKKT_AMALG_Z": "0.9"},
+}
+
+
+@pytest.mark.parametrize("path", sorted(BATCH_PATHS))
 @pytest.mark.parametrize("name", NAMES)
 def test_batched_matches_golden(name, path, monkeypatch):
-    """Both batched paths: system-per-CTA stream solve (default where the
-    solve vector fits shared memory) and lane-per-system (HYKKT_BATCH_PATH=lane)."""
-    if path == "lane":
-        monkeypatch.setenv("HYKKT_BATCH_PATH", "lane")
+    """Every batched path: system-per-CTA stream solve (default where the
+    solve vector fits shared memory), lane-per-system (HYKKT_BATCH_PATH=lane),
+    the opt-in per-system factorization and amalgamated supernodes."""
+    for k, v in BATCH_PATHS[path].items():
+        monkeypatch.setenv(k, v)
     s, cfg, perm, want = load(name)
     dev = Device(0)
     dev.analyze(s, perm)
@@ -108,6 +118,8 @@ VARIANTS = {
     "cta_everything": {"HYKKT_MF_BIG": "1", "HYKKT_TRSV_WIDE": "1", "HYKKT_TRSV_BOTTOM_MIN": "100000000"},
     "bottom_levels": {"HYKKT_TRSV_BOTTOM_MIN": "1"},
     "left_looking_factor": {"HYKKT_FACTOR": "ll"},
+    # relaxed amalgamation (explicit zeros in the panels, analyze.cpp)
+    "amalgamated": {"HYKKT_AMALG_W": "16", "HYKKT_AMALG_Z": "0.9"},
 }
 
 

@@ -20,7 +20,7 @@ out = np.zeros(6 * ns, np.uint64)
 for _ in range(3):
     _lib.check(L.hykkt_debug_trsv_trace(dev.h, out.ctypes.data_as(C.POINTER(C.c_uint64))))
 end, start, ready = out[:2 * ns].astype(np.int64), out[2 * ns:4 * ns].astype(np.int64), out[4 * ns:].astype(np.int64)
-t0 = start.min(); end = (end - t0) / 1e3; start = (start - t0) / 1e3; ready = np.where(ready > 0, (ready - t0) / 1e3, np.nan)
+t0 = start[start > 0].min(); end = (end - t0) / 1e3; start = (start - t0) / 1e3; ready = np.where(ready > 0, (ready - t0) / 1e3, np.nan)
 width = np.diff(first)
 fend = np.zeros(ns); fstart = np.zeros(ns); bend = np.zeros(ns); bstart = np.zeros(ns); fready = np.zeros(ns); bready = np.zeros(ns)
 fend[order] = end[:ns]; fstart[order] = start[:ns]; fready[order] = ready[:ns]; bready[order[::-1]] = ready[ns:]
