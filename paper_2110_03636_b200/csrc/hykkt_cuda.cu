@@ -31,6 +31,7 @@
 #include "kernels_sys.cuh"
 #include "kernels_mf.cuh"
 #include "kernels_metrics.cuh"
+#include "kernels_cluster.cuh"
 #include "sysplan.hpp"
 
 namespace hykkt {
@@ -122,6 +123,19 @@ struct hykkt_context {
   int tr_nwid = 0, tr_nnar = 0, tr_nbot = 0;
   hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
   hykkt::DBuf<unsigned char> tr_bot_wide;
+  // Q-form wide supernodes (kernels_solve.cuh qslice_fwd / qslice_bwd / k_qform)
+  hykkt::DBuf<double> q_buf;
+  hykkt::DBuf<long long> q_off;
+  hykkt::DBuf<int> q_items, q_sf, q_sb;
+  int q_nrows = 0, q_nsf = 0, q_nsb = 0;
+  long long panel_ver = 0, q_ver = -1;
+  // single-system solve on one thread-block cluster (kernels_cluster.cuh)
+  int cl_on = 0, cl_ctas = 0, cl_nlev = 0;
+  hykkt::DBuf<int> cl_lv_ptr, cl_lv_sn, cl_desc, cl_gat4, cl_wl, cl_wptr, cl_rec, cl_vmap;
+  hykkt::DBuf<double> cl_vals;
+  int cl_nvals = 0;
+  hykkt::DBuf<double> cl_bt;
+  hykkt::DBuf<unsigned long long> cl_stamps;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
   bool ruiz_rows_built = false;
@@ -320,6 +334,8 @@ int occupancy_blocks(Ctx& c, const void* fn, std::size_t smem = 0) {
   return std::max(1, std::min(per_sm, cap)) * c.num_sms;
 }
 
+int pick_cluster_ctas(Ctx& c);
+
 void init_ctx(Ctx& c, int device) {
   c.device = device;
   CK(cudaSetDevice(device));
@@ -332,9 +348,7 @@ void init_ctx(Ctx& c, int device) {
   c.coop_mf_blocks = occupancy_blocks(c, (const void*)dev::k_mf_factor);
   c.coop_trsv_blocks = occupancy_blocks(c, (const void*)dev::k_trsv);
   {
-    int minb = 2;
-    if (const char* e = std::getenv("HYKKT_CG_MINB")) minb = std::atoi(e);
-    c.cg_fn = minb >= 4 ? (const void*)dev::k_cg<4> : minb == 3 ? (const void*)dev::k_cg<3> : (const void*)dev::k_cg<2>;
+    c.cg_fn = (const void*)dev::k_cg<2>;  // 2 CTAs per SM (B200 sweep of 2 / 3 / 4 in round 1)
   }
   c.coop_cg_blocks = occupancy_blocks(c, c.cg_fn);
   c.coop_ruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_ruiz), 2 * c.num_sms);
@@ -349,6 +363,14 @@ void init_ctx(Ctx& c, int device) {
   }
   c.coop_bruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::kb_ruiz), 2 * c.num_sms);
   c.coop_bruiz_rows_blocks = occupancy_blocks(c, (const void*)dev::kb_ruiz_rows);
+  {
+    unsigned ns = 16, mx = 16;
+    if (const char* e = std::getenv("HYKKT_POLL_NS")) ns = static_cast<unsigned>(std::max(0, std::atoi(e)));
+    if (const char* e = std::getenv("HYKKT_POLL_MAX_NS")) mx = static_cast<unsigned>(std::max(0, std::atoi(e)));
+    mx = std::max(mx, ns);
+    CK(cudaMemcpyToSymbol(dev::g_poll_ns, &ns, sizeof(ns)));
+    CK(cudaMemcpyToSymbol(dev::g_poll_max_ns, &mx, sizeof(mx)));
+  }
   c.barrier.alloc(2);
   CK(cudaMemsetAsync(c.barrier.p, 0, 2 * sizeof(unsigned), c.stream));
   c.status.alloc(1);
@@ -385,6 +407,178 @@ void level_tasks(const SupernodalPlan& s, Pred big, std::vector<int>& tp, std::v
   }
 }
 
+// Level lists of the cluster solve (kernels_cluster.cuh): per level of the
+// supernode tree, thread tasks (w <= 4, rows <= 16, on levels with at least
+// HYKKT_CL_THREAD_MIN supernodes), warp tasks (w <= 32, rows <= kClRows,
+// panel <= kClVals) and whole-CTA tasks (the rest).  Warp tasks go to
+// per-warp lists in level order (round robin over the cluster's warps; a
+// run of levels holding a single parent chain of warp tasks is merged into
+// one level on one warp), each with an int record (4-slot gathers, rows
+// below) and a value record (panel, reciprocal diagonal) rebuilt from the
+// factor by k_cl_remap.
+void build_cluster_plan(Ctx& c) {
+  const SupernodalPlan& s = c.sp;
+  c.cl_nlev = 0;
+  if (const char* e = std::getenv("HYKKT_CLUSTER")) c.cl_on = std::atoi(e) != 0;
+  if (!c.cl_on || s.nsup == 0) return;
+  if (s.max_nrows > dev::kWideMaxRows) return;  // CTA tasks stage their rows in shared memory
+  c.cl_ctas = pick_cluster_ctas(c);
+  const int nwarps = c.cl_ctas * dev::kClWarps;
+  int thread_min = 1024;
+  if (const char* e = std::getenv("HYKKT_CL_THREAD_MIN")) thread_min = std::atoi(e);
+  const bool chain_on = !std::getenv("HYKKT_CL_CHAIN") || std::atoi(std::getenv("HYKKT_CL_CHAIN")) != 0;
+  // levels of s.order
+  std::vector<std::vector<int>> levels;
+  for (idx q = 0; q < s.nsup;) {
+    const int lev = s.sn_level[s.order[q]];
+    levels.emplace_back();
+    for (; q < s.nsup && s.sn_level[s.order[q]] == lev; ++q) levels.back().push_back(s.order[q]);
+  }
+  auto kind = [&](int sn, bool many) {  // 0 thread, 1 warp, 2 CTA
+    const int w = s.sn_first[sn + 1] - s.sn_first[sn], nr = s.sn_nrows[sn];
+    if (w > 32 || nr > dev::kClRows || w * nr > dev::kClVals) return 2;
+    if (many && w <= 4 && nr <= 16) return 0;
+    return 1;
+  };
+  std::vector<int> lv, csn, desc, rec, vmap;
+  std::vector<std::vector<int>> wlist(nwarps);  // 8 ints per entry
+  auto push_desc = [&](int sn) {
+    const int f = s.sn_first[sn], w = s.sn_first[sn + 1] - f, nr = s.sn_nrows[sn];
+    desc.insert(desc.end(), {sn, f, w | (nr << 16), static_cast<int>(s.sn_off[sn]), s.u_off[sn],
+                             s.sn_rows_ptr[sn], 0, 0});
+  };
+  auto push_warp = [&](int sn, int gw, int level) {
+    const int f = s.sn_first[sn], w = s.sn_first[sn + 1] - f, nr = s.sn_nrows[sn], rp = s.sn_rows_ptr[sn];
+    const int roff = static_cast<int>(rec.size()), voff = static_cast<int>(vmap.size());
+    for (int q = 0; q < nr; ++q) {
+      const int t = rp + q, e0 = s.gat_ptr[t], e1 = s.gat_ptr[t + 1];
+      int g[4] = {-1, -1, -1, -1};
+      if (e1 - e0 <= 4) {
+        for (int e = e0; e < e1; ++e) g[e - e0] = s.gat_idx[e];
+      } else {
+        for (int k = 0; k < 3; ++k) g[k] = s.gat_idx[e0 + k];
+        g[3] = -2 - (e0 + 3);
+      }
+      rec.insert(rec.end(), g, g + 4);
+    }
+    for (int q = w; q < nr; ++q) rec.push_back(s.sn_rows[rp + q]);
+    while (rec.size() % 4) rec.push_back(0);
+    for (int k = 0; k < w; ++k)
+      for (int q = 0; q < nr; ++q) vmap.push_back(2 * static_cast<int>(s.sn_off[sn] + k * nr + q) + (q == k ? 1 : 0));
+    if (vmap.size() % 2) vmap.push_back(-1);
+    wlist[gw].insert(wlist[gw].end(), {roff, voff, w | (nr << 16), s.u_off[sn], f, level, rp, 0});
+  };
+  int nl = 0;
+  for (std::size_t L = 0; L < levels.size();) {
+    const auto& g = levels[L];
+    const bool many = static_cast<int>(g.size()) >= thread_min;
+    // a chain: consecutive single-warp-task levels, each task the parent's child
+    std::size_t L2 = L + 1;
+    if (chain_on && g.size() == 1 && kind(g[0], false) == 1) {
+      while (L2 < levels.size() && levels[L2].size() == 1 && kind(levels[L2][0], false) == 1 &&
+             s.sn_parent[levels[L2 - 1][0]] == levels[L2][0])
+        ++L2;
+    }
+    lv.push_back(static_cast<int>(desc.size() / 8));
+    if (L2 > L + 1) {
+      for (std::size_t k = L; k < L2; ++k) push_warp(levels[k][0], 0, nl);
+    } else {
+      int rr = 0;
+      for (int sn : g) {
+        const int kd = kind(sn, many);
+        if (kd == 0) push_desc(sn);
+        else if (kd == 2) csn.push_back(sn);
+        else push_warp(sn, (rr++) % nwarps, nl);
+      }
+    }
+    lv.push_back(static_cast<int>(desc.size() / 8));  // thread tasks end
+    lv.push_back(static_cast<int>(desc.size() / 8));  // (unused)
+    lv.push_back(static_cast<int>(csn.size()));       // CTA tasks end (start: previous level's end)
+    ++nl;
+    L = L2;
+  }
+  c.cl_nlev = nl;
+  std::vector<int> wl, wptr{0};
+  for (auto& v : wlist) {
+    wl.insert(wl.end(), v.begin(), v.end());
+    wptr.push_back(static_cast<int>(wl.size() / 8));
+  }
+  std::vector<int> g4(4 * static_cast<std::size_t>(std::max(1, s.sn_rows_ptr.back())), -1);
+  for (int t = 0; t < s.sn_rows_ptr.back(); ++t) {
+    const int e0 = s.gat_ptr[t], e1 = s.gat_ptr[t + 1];
+    if (e1 - e0 <= 4) {
+      for (int e = e0; e < e1; ++e) g4[4 * t + (e - e0)] = s.gat_idx[e];
+    } else {
+      for (int k = 0; k < 3; ++k) g4[4 * t + k] = s.gat_idx[e0 + k];
+      g4[4 * t + 3] = -2 - (e0 + 3);
+    }
+  }
+  rec.resize(rec.size() + 8, 0);  // copy over-reach
+  vmap.resize(vmap.size() + 2, -1);
+  c.cl_lv_ptr.upload(lv, c.stream);
+  c.cl_desc.upload(desc.empty() ? std::vector<int>(8, 0) : desc, c.stream);
+  c.cl_lv_sn.upload(csn.empty() ? std::vector<int>{0} : csn, c.stream);
+  c.cl_gat4.upload(g4, c.stream);
+  c.cl_wl.upload(wl.empty() ? std::vector<int>(8, 0) : wl, c.stream);
+  c.cl_wptr.upload(wptr, c.stream);
+  c.cl_rec.upload(rec, c.stream);
+  c.cl_vmap.upload(vmap, c.stream);
+  c.cl_vals.alloc(vmap.size());
+  c.cl_nvals = static_cast<int>(vmap.size());
+  c.cl_bt.alloc(std::max<idx>(1, s.n));
+  c.cl_stamps.alloc(2 * c.cl_nlev + 2 + 768);
+}
+
+std::size_t cluster_smem() { return sizeof(dev::ClSmem); }
+
+// Cluster size for k_cluster_solve: HYKKT_CL_CTAS (default 16, the
+// non-portable maximum), reduced until the device can host one cluster.
+int pick_cluster_ctas(Ctx& c) {
+  int want = 16;
+  if (const char* e = std::getenv("HYKKT_CL_CTAS")) want = std::max(1, std::min(16, std::atoi(e)));
+  const void* fn = (const void*)dev::k_cluster_solve;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cluster_smem())));
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  for (int cs = want; cs >= 1; cs /= 2) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(dev::kClThreads);
+    cfg.dynamicSmemBytes = cluster_smem();
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n >= 1) return cs;
+    cudaGetLastError();
+  }
+  throw CudaError("no cluster configuration fits k_cluster_solve");
+}
+
+void launch_cluster(Ctx& c, dev::ClArgs& a) {
+  if (c.cl_nvals > 0) {  // warp-task value records from the current factor
+    dev::k_cl_remap<<<(c.cl_nvals + kThreads - 1) / kThreads, kThreads, 0, c.stream>>>(c.cl_nvals, c.cl_vmap.p,
+                                                                                     c.panel.p, c.cl_vals.p);
+    check_launch(c);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(c.cl_ctas);
+  cfg.blockDim = dim3(dev::kClThreads);
+  cfg.dynamicSmemBytes = cluster_smem();
+  cfg.stream = c.stream;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = c.cl_ctas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, dev::k_cluster_solve, a));
+  c.launches++;
+}
 
 void upload_plan(Ctx& c, const CscPattern& src_pattern) {
   const SupernodalPlan& s = c.sp;
@@ -527,12 +721,49 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
       const long long w = s.sn_first[sn + 1] - s.sn_first[sn];
       (s.sn_nrows[sn] <= dev::kWideMaxRows && w * s.sn_nrows[sn] >= wide ? wid : nar).push_back(sn);
     }
+    // Q-form: every wide supernode (w <= kQMaxW) gets Q = [L_ss^-1; L_below
+    // L_ss^-1] after each factorization and runs as independent row /
+    // column slices over the wide CTAs (HYKKT_QFORM=0 keeps whole-supernode
+    // substitution tasks)
+    c.q_nrows = c.q_nsf = c.q_nsb = 0;
+    {
+      const char* e = std::getenv("HYKKT_QFORM");
+      bool on = e ? std::atoi(e) != 0 : false;
+      for (int sn : wid)
+        if (s.sn_first[sn + 1] - s.sn_first[sn] > dev::kQMaxW) on = false;
+      if (on && !wid.empty()) {
+        std::vector<long long> qo(s.nsup, -1);
+        std::vector<int> items, sf, sb;
+        long long tot = 0;
+        for (int sn : wid) {
+          const int w = s.sn_first[sn + 1] - s.sn_first[sn], nr = s.sn_nrows[sn];
+          qo[sn] = tot;
+          tot += static_cast<long long>(w) * nr;
+          for (int qr = 0; qr < nr; ++qr) items.insert(items.end(), {sn, qr});
+          for (int r0 = 0; r0 < nr; r0 += 32) sf.insert(sf.end(), {sn, r0, std::min(r0 + 32, nr), 0});
+        }
+        for (auto it = wid.rbegin(); it != wid.rend(); ++it) {
+          const int sn = *it, w = s.sn_first[sn + 1] - s.sn_first[sn];
+          for (int c0 = 0; c0 < w; c0 += kThreads / 32) sb.insert(sb.end(), {sn, c0, std::min(c0 + kThreads / 32, w), 0});
+        }
+        c.q_buf.alloc(static_cast<std::size_t>(tot));
+        c.q_off.upload(qo, st);
+        c.q_items.upload(items, st);
+        c.q_sf.upload(sf, st);
+        c.q_sb.upload(sb, st);
+        c.q_nrows = static_cast<int>(items.size() / 2);
+        c.q_nsf = static_cast<int>(sf.size() / 4);
+        c.q_nsb = static_cast<int>(sb.size() / 4);
+        c.q_ver = -1;
+      }
+    }
     c.tr_wid.upload(wid.empty() ? std::vector<int>{0} : wid, st);
     c.tr_nar.upload(nar.empty() ? std::vector<int>{0} : nar, st);
     c.tr_nwid = static_cast<int>(wid.size());
     c.tr_nnar = static_cast<int>(nar.size());
     c.tr_pos.upload(pos, st);
   }
+  build_cluster_plan(c);
   CK(cudaMemsetAsync(c.fac_done.p, 0, sizeof(int) * std::max<idx>(1, s.nsup), st));
   c.epoch = 0;
   c.have_plan = true;
@@ -559,6 +790,25 @@ StatusBlock read_status(Ctx& c) {
   CK(cudaMemcpyAsync(&sb, c.status.p, sizeof(sb), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   if (sb.abort) {
+    unsigned long long fa = 0;
+    cudaMemcpyFromSymbol(&fa, dev::g_poll_fail_addr, sizeof(fa));
+    if (std::getenv("HYKKT_DEBUG") && fa) {
+      const auto* p = reinterpret_cast<const double*>(fa);
+      auto in = [&](const hykkt::DBuf<double>& b) { return p >= b.p && p < b.p + b.n; };
+      const char* which = in(c.y) ? "y" : in(c.xsol) ? "x" : in(c.ubuf) ? "u" : "?";
+      long long off = in(c.y) ? p - c.y.p : in(c.xsol) ? p - c.xsol.p : in(c.ubuf) ? p - c.ubuf.p : -1;
+      int owner = -1;
+      if (which[0] == 'u') {
+        for (idx k = 0; k < c.sp.nsup; ++k)
+          if (c.sp.u_off[k] <= off && off < c.sp.u_off[k + 1]) owner = static_cast<int>(k);
+      } else if (off >= 0) {
+        owner = c.sp.sn_of[off];
+      }
+      unsigned who = 0;
+      cudaMemcpyFromSymbol(&who, dev::g_poll_fail_who, sizeof(who));
+      std::fprintf(stderr, "[hykkt] first timed-out wait: %s[%lld] (supernode %d, parent %d) by block %u thread %u\n",
+                   which, off, owner, owner >= 0 ? c.sp.sn_parent[owner] : -1, who >> 10, who & 1023);
+    }
     throw TimeoutError("device wait timed out (dependency deadlock or lost wake-up); results discarded");
   }
   return sb;
@@ -576,6 +826,7 @@ int factor_attempt(Ctx& c, const double* src, double delta1, double floor_abs,
                    const double* maxdiag, double floor_rel) {
   const SupernodalPlan& s = c.sp;
   CK(cudaMemsetAsync(c.panel.p, 0, sizeof(double) * std::max<idx>(1, s.panel_size), c.stream));
+  c.panel_ver++;
   const int nsrc = static_cast<int>(s.src_to_panel.size());
   if (nsrc > 0) {
     dev::k_scatter<<<blocks_for(nsrc), kThreads, 0, c.stream>>>(
@@ -639,6 +890,7 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.rhs.jval = nullptr;
   ta.bar = dev::GridBarrier{c.barrier.p, c.barrier.p + 1};
   ta.trace = nullptr;
+  ta.pstamp = nullptr;
   ta.wid_sn = c.tr_wid.p;
   ta.nwid = c.tr_nwid;
   ta.nar_sn = c.tr_nar.p;
@@ -649,7 +901,8 @@ dev::TrsvArgs trsv_args(Ctx& c) {
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
     nwc = std::min({nwc, c.tr_nwid, std::max(1, c.coop_cg_blocks / 2)});
     ta.nwc = c.tr_nwid > 0 ? nwc : 0;
-    ta.pre_wait = 10;  // narrow tasks poll their own values (B200 sweep; the general ones need the pre-wait)
+    ta.pre_wait = 10;  // general tasks poll one value per dependency first, narrow ones poll their own values
+                       // (r02 A/B on the current kernel: 15 = all pre-wait is 10-14 % slower at C1-C4)
     if (const char* e = std::getenv("HYKKT_TRSV_PREWAIT")) ta.pre_wait = std::atoi(e);
   }
   ta.pos = c.tr_pos.p;
@@ -657,14 +910,62 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.bot_ptr = c.tr_bot_ptr.p;
   ta.bot_sn = c.tr_bot_sn.p;
   ta.bot_wide = c.tr_bot_wide.p;
+  ta.bt = nullptr;
+  ta.q = c.q_buf.p;
+  ta.qoff = c.q_off.p;
+  ta.qs_f = reinterpret_cast<const int4*>(c.q_sf.p);
+  ta.nqf = c.q_nsf;
+  ta.qs_b = reinterpret_cast<const int4*>(c.q_sb.p);
+  ta.nqb = c.q_nsb;
   return ta;
 }
 
 // One H^-1 application; the result stays in c.xsol (permuted order) and,
 // when x_out is given, is scattered to original order there.
+dev::ClArgs cluster_args(Ctx& c) {
+  dev::ClArgs a{};
+  a.tr = trsv_args(c);
+  a.tr.pre_wait = 0;
+  a.tr.nbot = 0;
+  a.tr.bt = c.cl_bt.p;
+  a.bt = c.cl_bt.p;
+  a.nlev = c.cl_nlev;
+  a.lv = c.cl_lv_ptr.p;
+  a.desc = reinterpret_cast<const int4*>(c.cl_desc.p);
+  a.cta_sn = c.cl_lv_sn.p;
+  a.gat4 = reinterpret_cast<const int4*>(c.cl_gat4.p);
+  a.wl = reinterpret_cast<const int4*>(c.cl_wl.p);
+  a.wl_ptr = c.cl_wptr.p;
+  a.rec = c.cl_rec.p;
+  a.vals = c.cl_vals.p;
+  a.stamps = std::getenv("HYKKT_CL_STAMPS") ? c.cl_stamps.p : nullptr;
+  return a;
+}
+
+// Q of the Q-form supernodes from the current factor (once per factor).
+void ensure_qform(Ctx& c) {
+  if (c.q_nrows == 0 || c.q_ver == c.panel_ver) return;
+  const int wpb = kThreads / 32;
+  dev::k_qform<<<(c.q_nrows + wpb - 1) / wpb, kThreads, 0, c.stream>>>(
+      c.q_nrows, reinterpret_cast<const int2*>(c.q_items.p), c.snplan(), c.panel.p, c.q_off.p, c.q_buf.p);
+  check_launch(c);
+  c.q_ver = c.panel_ver;
+}
+
 void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, double* x_out) {
   const SupernodalPlan& s = c.sp;
   if (s.nsup == 0) return;
+  if (c.cl_nlev > 0) {
+    dev::ClArgs a = cluster_args(c);
+    a.tr.x_out = x_out;
+    a.tr.rhs.b = b;
+    a.tr.rhs.u = u;
+    a.tr.rhs.jval = jval;
+    a.mode = 0;
+    launch_cluster(c, a);
+    return;
+  }
+  ensure_qform(c);
   dev::TrsvArgs ta = trsv_args(c);
   ta.x_out = x_out;
   ta.rhs.b = b;
@@ -694,8 +995,30 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   a.thr = cfg.small_quadratic_threshold;
   a.max_iter = cfg.cg_max_iter;
   a.res = &c.status.p->cg;
-  a.tickets = fresh_tickets(c, 2 * (cfg.cg_max_iter + 2));
   if (c.sp.nsup == 0 && c.kp.mc > 0) throw StateError("empty factor with constraints");
+  if (c.cl_nlev > 0) {
+    dev::ClArgs ca = cluster_args(c);
+    ca.tr.rhs = a.tr.rhs;
+    ca.mode = 1;
+    ca.mc = a.mc;
+    ca.jcsr_rp = a.jcsr_rp;
+    ca.jcsr_ci_perm = a.jcsr_ci_perm;
+    ca.jcsr = a.jcsr;
+    ca.rhs = a.rhs;
+    ca.x = a.x;
+    ca.r = a.r;
+    ca.p = a.p;
+    ca.q = a.q;
+    ca.delta2 = a.delta2;
+    ca.tol = a.tol;
+    ca.thr = a.thr;
+    ca.max_iter = a.max_iter;
+    ca.res = a.res;
+    launch_cluster(c, ca);
+    return read_status(c).cg;
+  }
+  ensure_qform(c);
+  a.tickets = fresh_tickets(c, 2 * (cfg.cg_max_iter + 2));
   coop_launch(c, c.cg_fn, c.coop_cg_blocks, &a);
   return read_status(c).cg;
 }
@@ -2587,6 +2910,52 @@ int hykkt_debug_plan(hykkt_t h, int32_t* order, int32_t* first, int32_t* nrows, 
 // Diagnostics: one traced H^-1 pass (b = r_hat_x of the last KKT solve);
 // out[t] / out[2 nsup + t] = end / start time (ns) of task t (t < nsup:
 // forward task of order[t]; else backward task of order[2 nsup - 1 - t]).
+// Diagnostics: one k_trsv pass (w solve) with per-CTA phase stamps
+// (8 per CTA: start, after rearm barrier, after the forward bottom levels,
+// task loop exit, after the backward bottom barrier, after backward bottom /
+// levels, -, end).  Returns the grid size in *nblk.
+int hykkt_debug_trsv_phases(hykkt_t h, uint64_t* out, int64_t cap, int64_t* nblk) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_factor || !c.have_kkt) throw StateError("needs a factored KKT system");
+    *nblk = c.coop_trsv_blocks;
+    if (cap < 8 * c.coop_trsv_blocks) return;
+    hykkt::DBuf<unsigned long long> st;
+    st.alloc(8 * c.coop_trsv_blocks);
+    CK(cudaMemset(st.p, 0, 8 * c.coop_trsv_blocks * sizeof(unsigned long long)));
+    ensure_qform(c);
+      dev::TrsvArgs ta = trsv_args(c);
+    ta.rhs.b = c.rhat.p;
+    ta.pstamp = st.p;
+    ta.ticket = fresh_tickets(c, 2);
+    coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
+    read_status(c);
+    CK(cudaMemcpy(out, st.p, 8 * c.coop_trsv_blocks * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
+// Diagnostics: the cluster solve's per-level end times of the last pass
+// (HYKKT_CL_STAMPS=1 at analysis), 2 * levels values (forward levels, then
+// backward), and the level lists' sizes (4 per level: thread, warp, CTA, 0).
+int hykkt_debug_cluster_stamps(hykkt_t h, uint64_t* out, int* sizes, int64_t cap, int64_t* nlev) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    *nlev = c.cl_nlev;
+    if (c.cl_nlev == 0 || cap < 2 * c.cl_nlev) return;
+    CK(cudaStreamSynchronize(c.stream));
+    if (cap < 2 * c.cl_nlev + 768) return;
+    CK(cudaMemcpy(out, c.cl_stamps.p, (2 * c.cl_nlev + 768) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    std::vector<int> lp(4 * c.cl_nlev);
+    CK(cudaMemcpy(lp.data(), c.cl_lv_ptr.p, lp.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int l = 0; l < c.cl_nlev; ++l) {
+      sizes[4 * l] = lp[4 * l + 1] - lp[4 * l];
+      sizes[4 * l + 1] = lp[4 * l + 2] - lp[4 * l + 1];
+      sizes[4 * l + 2] = lp[4 * l + 3] - (l ? lp[4 * l - 1] : 0);
+      sizes[4 * l + 3] = 0;
+    }
+  });
+}
+
 int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
   return guarded([&] {
     Ctx& c = ctx(h);
@@ -2594,7 +2963,8 @@ int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
     const idx ns = c.sp.nsup;
     hykkt::DBuf<unsigned long long> tr;
     tr.alloc(6 * ns);
-    dev::TrsvArgs ta = trsv_args(c);
+    ensure_qform(c);
+      dev::TrsvArgs ta = trsv_args(c);
     ta.rhs.b = c.rhat.p;
     ta.trace = tr.p;
     ta.ticket = fresh_tickets(c, 2);
@@ -2655,6 +3025,7 @@ void set_factor(Ctx& c, const double* l_values) {
   std::vector<double> pan(std::max<idx>(1, s.panel_size), 0.0);
   for (std::size_t q = 0; q < s.l_to_panel.size(); ++q) pan[s.l_to_panel[q]] = l_values[q];
   CK(cudaMemcpyAsync(c.panel.p, pan.data(), s.panel_size * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  c.panel_ver++;
   CK(cudaStreamSynchronize(c.stream));
   c.have_factor = true;
 }

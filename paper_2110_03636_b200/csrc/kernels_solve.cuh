@@ -43,18 +43,37 @@ struct SolveRhs {
 // its own completion flag — no per-task flags, no fences on the hot path.
 constexpr long long kUnset = 0x7FF4DEADBEEF0001ll;
 
+__device__ unsigned long long g_poll_fail_addr = 0;  // diagnostics: first value whose wait timed out
+__device__ unsigned g_poll_fail_who = 0;              // and its waiter (block << 10 | thread)
+
+// Raises the abort flag for a wait that exceeded the spin budget and
+// records the first such wait (read by the host when HYKKT_DEBUG is set).
+__device__ __noinline__ void poll_timed_out(const double* p, int* abort) {
+  if (atomicCAS(&g_poll_fail_addr, 0ull, reinterpret_cast<unsigned long long>(p)) == 0ull)
+    g_poll_fail_who = (blockIdx.x << 10) | threadIdx.x;
+  atomicExch(abort, 1);
+}
+
+// Poll back-off (ns): first sleep, doubling up to the cap (HYKKT_POLL_NS /
+// HYKKT_POLL_MAX_NS, set once per context; 16 / 16 by default: longer
+// sleeps or a back-off measured no gain at C1-C4, r02 ab3).
+__device__ unsigned g_poll_ns = 16, g_poll_max_ns = 16;
+
 __device__ __forceinline__ double poll_value(const double* p, int* abort) {
   double v = ldcg(p);
   if (__double_as_longlong(v) != kUnset) return v;
   const long long t0 = clock64();
+  unsigned ns = g_poll_ns;
+  const unsigned cap = g_poll_max_ns;
   for (unsigned it = 1;; ++it) {
-    __nanosleep(16);
+    __nanosleep(ns);
+    ns = min(2 * ns, cap);
     v = ldcg(p);
     if (__double_as_longlong(v) != kUnset) return v;
     if ((it & 255u) == 0u) {
       if (ld_relaxed(abort)) return 0.0;
       if (clock64() - t0 > kSpinBudget) {
-        atomicExch(abort, 1);
+        poll_timed_out(p, abort);
         return 0.0;
       }
     }
@@ -80,6 +99,7 @@ struct TrsvArgs {
   GridBarrier bar;
   unsigned* ticket;           // task counter of this pass (zero on entry)
   unsigned long long* trace;  // diagnostics: per-task end / start times (ns)
+  unsigned long long* pstamp; // diagnostics: per-CTA phase times of k_trsv (8 per CTA), or null
   // task streams (trsv_pass): wide supernodes for the first nwc CTAs,
   // narrow ones for the warps of the others; ticket[0] / ticket[1]
   const int* wid_sn;
@@ -98,13 +118,26 @@ struct TrsvArgs {
   const int* bot_ptr;         // nbot + 1
   const int* bot_sn;
   const unsigned char* bot_wide;  // per bottom level: 1 -> (w <= 8, nrows <= 32) variant
+  // precomputed right-hand side of every permuted row (kernels_cluster.cuh),
+  // null: rhs_at forms b - J^T u on the fly
+  const double* bt;
+  // Q-form wide supernodes (qslice_fwd / qslice_bwd): Q = [L_ss^-1;
+  // L_below L_ss^-1] (nrows x w, column-major at qoff[sn]); the wide stream
+  // then runs independent row slices (forward, int4 {sn, r0, r1, 0}) and
+  // column slices (backward, {sn, c0, c1, 0}) instead of whole supernodes
+  const double* q;
+  const long long* qoff;
+  const int4* qs_f;
+  int nqf;
+  const int4* qs_b;
+  int nqb;
 };
 
 constexpr int kWideMaxRows = 2048;  // wide (CTA) solve tasks stage nrows doubles in shared memory
 constexpr int kWarpRows = kWideMaxRows / 8;  // narrow-task CTAs: each warp's slice of the same buffer
 struct TrsvSmem {
   double a[kWideMaxRows];
-  double t[32];
+  double t[64];  // bwd_cta: one partial per (column < 32) x slice; sized for 512-thread CTAs
   int task;  // wide-stream ticket value broadcast to the CTA
 };
 
@@ -122,7 +155,7 @@ __device__ __forceinline__ void reset_unset(double* v, int n) {
 
 // Right-hand side entry of permuted row i: b[perm i] and/or J^T u in the
 // reference's spmv(J, u, transpose) order (csc_matrix.cpp:255-261).
-__device__ __forceinline__ double rhs_at(const TrsvArgs& a, int i) {
+__device__ __forceinline__ double rhs_raw(const TrsvArgs& a, int i) {
   const int o = a.s.perm[i];
   double bi = a.rhs.b ? a.rhs.b[o] : 0.0;
   if (a.rhs.u) {
@@ -133,6 +166,10 @@ __device__ __forceinline__ double rhs_at(const TrsvArgs& a, int i) {
     bi = a.rhs.b ? __dsub_rn(bi, t) : t;
   }
   return bi;
+}
+
+__device__ __forceinline__ double rhs_at(const TrsvArgs& a, int i) {
+  return a.bt ? ldcg(a.bt + i) : rhs_raw(a, i);
 }
 
 // Sum of u[gat_idx[g]] for g in [gb, ge) in list order, four loads in
@@ -507,6 +544,126 @@ __device__ void bwd_cta(const TrsvArgs& a, TrsvSmem& S, int sn) {
   }
 }
 
+// Q-form forward row slice [r0, r1) (<= 32 rows) of wide supernode sn:
+// a = b - (children's contributions) on the w own rows (every slice forms
+// it), then out_q = sum_k Q[q,k] a_k for its rows, split over the CTA's
+// warps by k ranges and combined in a fixed order: own rows -> y, rows
+// below -> u_sn (children's contributions to the row added).  Slices of one
+// supernode are independent (no intra-supernode synchronisation).
+__device__ void qslice_fwd(const TrsvArgs& a, TrsvSmem& S, int sn, int r0, int r1) {
+  const SnPlan& s = a.s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn], rp = s.rows_ptr[sn];
+  const double* Q = a.q + a.qoff[sn];
+  double* A = S.a;  // w own-row values, then the partial sums
+  for (int qq = tid; qq < w; qq += blockDim.x) {
+    double g = 0.0;
+    for (int e = __ldg(s.gat_ptr + rp + qq), e1 = __ldg(s.gat_ptr + rp + qq + 1); e < e1; ++e)
+      g += load_ready(a.u + __ldg(s.gat_idx + e), a.abort);
+    A[qq] = rhs_at(a, f + qq) - g;
+  }
+  __syncthreads();
+  const int q = r0 + lane;
+  const bool row = q < r1;
+  const int kb = (w * wid) / nwarp, ke = (w * (wid + 1)) / nwarp;
+  double t0 = 0.0, t1 = 0.0;
+  int k = kb;
+  for (; k + 2 <= ke; k += 2) {
+    if (row) {
+      t0 = fma(__ldg(Q + static_cast<long long>(k) * nr + q), A[k], t0);
+      t1 = fma(__ldg(Q + static_cast<long long>(k + 1) * nr + q), A[k + 1], t1);
+    }
+  }
+  if (k < ke && row) t0 = fma(__ldg(Q + static_cast<long long>(k) * nr + q), A[k], t0);
+  double* part = A + ((w + 1) & ~1);  // [nwarp][32]
+  part[wid * 32 + lane] = t0 + t1;
+  __syncthreads();
+  if (wid == 0 && row) {
+    double out = 0.0;
+    for (int j = 0; j < nwarp; ++j) out += part[j * 32 + lane];
+    if (q < w) {
+      stcg(a.y + f + q, out);
+    } else {
+      double g = 0.0;
+      for (int e = __ldg(s.gat_ptr + rp + q), e1 = __ldg(s.gat_ptr + rp + q + 1); e < e1; ++e)
+        g += load_ready(a.u + __ldg(s.gat_idx + e), a.abort);
+      stcg(a.u + s.u_off[sn] + q - w, g + out);
+    }
+  }
+}
+
+// Q-form backward column slice [c0, c1) (<= one column per warp):
+// v = [y_own; -x_below] (staged once per slice), x_c = sum_q Q[q,c] v_q.
+__device__ void qslice_bwd(const TrsvArgs& a, TrsvSmem& S, int sn, int c0, int c1) {
+  const SnPlan& s = a.s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const int* R = s.rows + s.rows_ptr[sn];
+  const double* Q = a.q + a.qoff[sn];
+  double* V = S.a;
+  for (int qq = tid; qq < nr; qq += blockDim.x)
+    V[qq] = qq < w ? load_ready(a.y + f + qq, a.abort) : -load_ready(a.x + __ldg(R + qq), a.abort);
+  __syncthreads();
+  for (int c = c0 + wid; c < c1; c += nwarp) {
+    const double* Qc = Q + static_cast<long long>(c) * nr;
+    double t0 = 0.0, t1 = 0.0;
+    int qq = lane;
+    for (; qq + 32 < nr; qq += 64) {
+      t0 = fma(__ldg(Qc + qq), V[qq], t0);
+      t1 = fma(__ldg(Qc + qq + 32), V[qq + 32], t1);
+    }
+    if (qq < nr) t0 = fma(__ldg(Qc + qq), V[qq], t0);
+    const double xc = warp_sum(t0 + t1);
+    if (lane == 0) {
+      stcg(a.x + f + c, xc);
+      if (a.x_out) a.x_out[s.perm[f + c]] = xc;
+    }
+  }
+  __syncthreads();
+}
+
+// Q = [L_ss^-1; L_below L_ss^-1] of the Q-form supernodes, one warp per
+// row q: Q[q,k] = (E[q,k] - sum_{j>k} Q[q,j] L[j,k]) / L[k,k] for
+// k = w-1 .. 0, E = [I; L_below] (the row of Q times L_ss equals E's row).
+// The row lives in registers (lane holds columns lane + 32 i).
+constexpr int kQMaxW = 512;
+__global__ void __launch_bounds__(256) k_qform(int nrows_total, const int2* __restrict__ items, SnPlan s,
+                                               const double* __restrict__ panel, const long long* __restrict__ qoff,
+                                               double* __restrict__ q) {
+  const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (item >= nrows_total) return;
+  const int2 it = items[item];
+  const int sn = it.x, qr = it.y;
+  const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
+  const double* P = panel + s.off[sn];
+  double* Qo = q + qoff[sn];
+  constexpr int NC = kQMaxW / 32;
+  double v[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) v[i] = 0.0;
+  for (int k = w - 1; k >= 0; --k) {
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int j = lane + 32 * i;
+      if (j > k && j < w) t = fma(v[i], __ldg(P + static_cast<long long>(k) * nr + j), t);
+    }
+    t = warp_sum(t);
+    const double e = qr < w ? (qr == k ? 1.0 : 0.0) : __ldg(P + static_cast<long long>(k) * nr + qr);
+    const double qk = (e - t) / __ldg(P + static_cast<long long>(k) * nr + k);
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      if (lane + 32 * i == k) v[i] = qk;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int j = lane + 32 * i;
+    if (j < w) Qo[static_cast<long long>(j) * nr + qr] = v[i];
+  }
+}
+
 // Bottom-level supernode, forward, one thread (w <= W, nrows <= NR): the
 // same arithmetic in the same order as fwd_task's narrow branch.
 template <int NR, int W>
@@ -618,8 +775,27 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
 __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int ns = a.s.nsup;
+  unsigned long long* ps = (a.pstamp && threadIdx.x == 0) ? a.pstamp + 8 * blockIdx.x : nullptr;
   if (a.nbot > 0) trsv_bottom(a, true);
-  if (static_cast<int>(blockIdx.x) < a.nwc) {
+  if (ps) ps[2] = global_ns();
+  if (static_cast<int>(blockIdx.x) < a.nwc && a.nqf > 0) {
+    // Q-form slices: forward row slices, then backward column slices
+    for (;;) {
+      if (tid == 0) S.task = static_cast<int>(atomicAdd(a.ticket, 1u));
+      __syncthreads();
+      const int t = S.task;
+      __syncthreads();
+      if (t >= a.nqf + a.nqb) break;
+      if (t < a.nqf) {
+        const int4 e = a.qs_f[t];
+        qslice_fwd(a, S, e.x, e.y, e.z);
+      } else {
+        const int4 e = a.qs_b[t - a.nqf];
+        qslice_bwd(a, S, e.x, e.y, e.z);
+      }
+      __syncthreads();
+    }
+  } else if (static_cast<int>(blockIdx.x) < a.nwc) {
     const int nt = a.nwid;
     for (;;) {
       if (tid == 0) S.task = static_cast<int>(atomicAdd(a.ticket, 1u));
@@ -648,10 +824,13 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
       if (a.trace && lane == 0) a.trace[slot] = global_ns();
     }
   }
+  if (ps) ps[3] = global_ns();
   if (a.nbot > 0) {
     grid_sync(a.bar, a.abort);
+    if (ps) ps[4] = global_ns();
     trsv_bottom(a, false);
   }
+  if (ps) ps[5] = global_ns();
 }
 
 __device__ __forceinline__ void rearm(const TrsvArgs& a) {
@@ -662,9 +841,13 @@ __device__ __forceinline__ void rearm(const TrsvArgs& a) {
 
 __global__ void __launch_bounds__(256) k_trsv(TrsvArgs a) {
   __shared__ TrsvSmem S;
+  unsigned long long* ps = (a.pstamp && threadIdx.x == 0) ? a.pstamp + 8 * blockIdx.x : nullptr;
+  if (ps) ps[0] = global_ns();
   rearm(a);
   grid_sync(a.bar, a.abort);
+  if (ps) ps[1] = global_ns();
   trsv_pass(a, S);
+  if (ps) ps[7] = global_ns();
 }
 
 // L values in forward row-list order (after a successful factorization).

@@ -120,6 +120,13 @@ VARIANTS = {
     "left_looking_factor": {"HYKKT_FACTOR": "ll"},
     # relaxed amalgamation (explicit zeros in the panels, analyze.cpp)
     "amalgamated": {"HYKKT_AMALG_W": "16", "HYKKT_AMALG_Z": "0.9"},
+    # opt-in: the whole solve on one thread-block cluster, level-synchronous
+    # (kernels_cluster.cuh); thread tasks on every level, and the default
+    "cluster": {"HYKKT_CLUSTER": "1"},
+    "cluster_threads": {"HYKKT_CLUSTER": "1", "HYKKT_CL_THREAD_MIN": "1"},
+    # opt-in: wide supernodes in Q-form (inverted diagonal block, row /
+    # column slices over the wide CTAs), every supernode wide
+    "qform": {"HYKKT_QFORM": "1", "HYKKT_TRSV_WIDE": "1", "HYKKT_TRSV_BOTTOM_MIN": "100000000"},
 }
 
 
