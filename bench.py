@@ -302,13 +302,34 @@ def main():
     nat_step_ms = hd.allmax(nat_ms / args.steps, world, f"cuda:{local}")
 
     # ---- end to end through the public API (pinned host buffers) ----
+    # sequential: upload (H2D) -> solve -> download (D2H) per step
     def e2e_loop():
         for st in range(args.steps):
             batch.upload(host_sets[st % N_SETS])
             batch.solve_resident(cfg)
             batch.download(host_out)
 
-    e2e_ms, _ = timed(e2e_loop)
+    e2e_seq_ms, _ = timed(e2e_loop)
+    e2e_seq_step_ms = hd.allmax(e2e_seq_ms / args.steps, world, f"cuda:{local}")
+    e2e_seq_value = hd.allsum(B, world, f"cuda:{local}") / (e2e_seq_step_ms / 1e3)
+
+    # pipelined (the reported e2e): hykkt_batch_upload_async of step k+1's
+    # inputs is issued before the solve of step k, and step k's outputs come
+    # back with hykkt_batch_download_async (double-buffered pinned host
+    # outputs); every step's H2D and D2H still happen inside the timed region
+    host_outs = [host_out, {n: pinned(a.shape) for n, a in host_out.items()}]
+
+    def e2e_pipe():
+        batch.upload_async(host_sets[0])
+        for st in range(args.steps):
+            if st + 1 < args.steps:
+                batch.upload_async(host_sets[(st + 1) % N_SETS])
+            batch.solve_resident(cfg)
+            batch.download_async(host_outs[st % 2])
+        batch.sync()
+
+    e2e_pipe()  # warm the staging buffers
+    e2e_ms, _ = timed(e2e_pipe)
     e2e_step_ms = hd.allmax(e2e_ms / args.steps, world, f"cuda:{local}")
     e2e_value = hd.allsum(B, world, f"cuda:{local}") / (e2e_step_ms / 1e3)
 
@@ -365,7 +386,13 @@ def main():
                    "supernode_levels": info["n_levels"], "analyze_s": analyze_s},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms,
+                "protocol": "pipelined public API: hykkt_batch_upload_async (pinned host -> device, next "
+                            "step's inputs issued before this step's solve) + hykkt_batch_solve_resident + "
+                            "hykkt_batch_download_async (device -> pinned host), hykkt_batch_sync at the end",
+                "sequential": {"value": e2e_seq_value, "ms_per_step": e2e_seq_step_ms,
+                               "protocol": "hykkt_batch_upload -> hykkt_batch_solve_resident -> "
+                                           "hykkt_batch_download per step"}},
         "gpu_launches": acc["launches"],
         "clocks": clk.summary(),
         "batch_phases_ms_per_step": {k: acc[k] / args.steps for k in (

@@ -203,6 +203,21 @@ int hykkt_batch_solve_resident(hykkt_t h, const hykkt_config_t* cfg,
 int hykkt_batch_download(hykkt_t h, double* dx, double* ds, double* dy,
                          double* dyd);
 
+/* --- pipelined batch copies (no reference counterpart: the reference's
+ * solve_sequence runs on host memory).  hykkt_batch_upload_async starts the
+ * host-to-device copy of a batch (same layout as hykkt_batch_upload; pinned
+ * host memory for true overlap) on the handle's copy stream and returns;
+ * the next hykkt_batch_solve_resident consumes the oldest pending upload (at
+ * most two pending), so the copy of batch k+1 overlaps the solve of batch k.
+ * hykkt_batch_download_async starts the device-to-host copy of the last
+ * solve's outputs (same layout as hykkt_batch_download) and returns; the
+ * buffers are complete after hykkt_batch_sync (or the next synchronous
+ * download).  A synchronous hykkt_batch_upload drops pending async uploads. */
+int hykkt_batch_upload_async(hykkt_t h, int64_t batch, const hykkt_values_t* values);
+int hykkt_batch_download_async(hykkt_t h, double* dx, double* ds, double* dy,
+                               double* dyd);
+int hykkt_batch_sync(hykkt_t h);
+
 /* --- device-resident values (a GPU-side interior-point
  * method never round-trips values over PCIe).  Same layouts as the host
  * entry points; the copies are device-to-device on the handle's stream.

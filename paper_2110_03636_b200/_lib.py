@@ -91,7 +91,7 @@ EXPORTS = [
     "hykkt_batch_solution_device", "hykkt_analyze_reduced", "hykkt_upload_reduced",
     "hykkt_upload_reduced_device", "hykkt_solve_reduced", "hykkt_assemble", "hykkt_hgamma_pattern",
     "hykkt_factor_ladder", "hykkt_chol_set_factor", "hykkt_chol_set_j", "hykkt_cg_schur",
-    "hykkt_set_option",
+    "hykkt_set_option", "hykkt_batch_upload_async", "hykkt_batch_download_async", "hykkt_batch_sync",
 ]
 
 
@@ -147,6 +147,9 @@ def lib() -> C.CDLL:
     L.hykkt_batch_upload.argtypes = [vp, C.c_int64, C.POINTER(Values)]
     L.hykkt_batch_solve_resident.argtypes = [vp, C.POINTER(Config), C.c_int, C.POINTER(Report)]
     L.hykkt_batch_download.argtypes = [vp, F64P, F64P, F64P, F64P]
+    L.hykkt_batch_upload_async.argtypes = [vp, C.c_int64, C.POINTER(Values)]
+    L.hykkt_batch_download_async.argtypes = [vp, F64P, F64P, F64P, F64P]
+    L.hykkt_batch_sync.argtypes = [vp]
     VPP = C.POINTER(C.c_void_p)
     I32P = C.POINTER(C.c_int32)
     L.hykkt_upload_values_device.argtypes = [vp, C.POINTER(Values)]

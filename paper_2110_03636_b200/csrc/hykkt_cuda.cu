@@ -123,6 +123,16 @@ struct hykkt_context {
   int tr_nwid = 0, tr_nnar = 0, tr_nbot = 0;
   hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
   hykkt::DBuf<unsigned char> tr_bot_wide;
+  // asynchronous batch copies (hykkt_batch_upload_async / _download_async):
+  // two staging slots of field-major host values filled on copy_stream, the
+  // next batched solve consumes the oldest; outputs staged for the D2H
+  cudaStream_t copy_stream = nullptr;
+  hykkt::DBuf<double> stage[2], out_stage;
+  long long stage_batch[2] = {0, 0};
+  cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+  cudaEvent_t out_ready = nullptr, out_free = nullptr;
+  bool stage_free_rec[2] = {false, false}, out_free_rec = false;
+  int stage_q[2] = {-1, -1}, stage_nq = 0, stage_next = 0;
   // Q-form wide supernodes (kernels_solve.cuh qslice_fwd / qslice_bwd / k_qform)
   hykkt::DBuf<double> q_buf;
   hykkt::DBuf<long long> q_off;
@@ -1567,7 +1577,7 @@ BatchLayout batch_layout(const KktPlan& k) {
 }
 
 int pow2_at_least(long long v);
-void batch_interleave_inputs(Ctx& c);
+void batch_interleave_inputs(Ctx& c, const double* src);
 
 void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v, bool device_only = false) {
   if (!c.have_kkt) throw StateError("hykkt_analyze must be called first");
@@ -1590,7 +1600,105 @@ void batch_upload(Ctx& c, idx batch, const hykkt_values_t* v, bool device_only =
   const int newBp = pow2_at_least(batch);
   if (newBp != c.bb.Bp) c.bb.flags_init = false;
   c.bb.Bp = newBp;
-  batch_interleave_inputs(c);
+  c.stage_nq = 0;  // a synchronous upload supersedes pending asynchronous ones
+  batch_interleave_inputs(c, c.bvals.p);
+}
+
+// Asynchronous host upload of the NEXT batch (pinned host memory for true
+// overlap): the field-major values go to a staging slot on the handle's copy
+// stream while the current batched solve runs; the next
+// hykkt_batch_solve_resident consumes the oldest pending upload (at most two
+// pending).  Slot reuse waits for its previous consumer.
+void ensure_copy_stream(Ctx& c) {
+  if (c.copy_stream) return;
+  CK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaEventCreateWithFlags(&c.stage_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.stage_free[i], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&c.out_ready, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c.out_free, cudaEventDisableTiming));
+}
+
+void batch_upload_async(Ctx& c, idx batch, const hykkt_values_t* v) {
+  if (!c.have_kkt) throw StateError("hykkt_analyze must be called first");
+  if (c.reduced) throw StateError("the batched path takes block-4x4 systems (hykkt_analyze)");
+  if (batch <= 0) throw InvalidArgument("batch must be positive");
+  if (!v) throw InvalidArgument("null values");
+  if (c.stage_nq >= 2) throw StateError("two asynchronous uploads already pending");
+  ensure_copy_stream(c);
+  const BatchLayout L = batch_layout(c.kp);
+  const int sl = c.stage_next;
+  c.stage_next ^= 1;
+  c.stage[sl].alloc(static_cast<std::size_t>(batch * L.total_per_sys));
+  if (c.stage_free_rec[sl]) CK(cudaStreamWaitEvent(c.copy_stream, c.stage_free[sl], 0));
+  const double* src[9] = {v->h_val, v->j_val, v->jd_val, v->d_x, v->d_s, v->r_tilde_x, v->r_s, v->r_y, v->r_yd};
+  idx off = 0;
+  for (int i = 0; i < 9; ++i) {
+    const idx n = batch * L.sizes[i];
+    copy_in(c.stage[sl].p + off, src[i], n, "batch value array", c.copy_stream, false);
+    off += n;
+  }
+  CK(cudaEventRecord(c.stage_ready[sl], c.copy_stream));
+  c.stage_batch[sl] = batch;
+  c.stage_q[c.stage_nq++] = sl;
+}
+
+// Consumes the oldest pending asynchronous upload (called at the start of a
+// batched solve): the solve stream waits for its copies, adopts the staged
+// buffer as the batch's values and interleaves it.
+void batch_take_async(Ctx& c) {
+  if (c.stage_nq == 0) return;
+  const int sl = c.stage_q[0];
+  c.stage_q[0] = c.stage_q[1];
+  --c.stage_nq;
+  const idx batch = c.stage_batch[sl];
+  CK(cudaStreamWaitEvent(c.stream, c.stage_ready[sl], 0));
+  const idx nout = c.kp.nx + c.kp.mc + 2 * c.kp.md;
+  c.bouts.alloc(static_cast<std::size_t>(batch * nout));
+  c.batch = batch;
+  c.batch_reports.assign(batch, hykkt_report_t{});
+  const int newBp = pow2_at_least(batch);
+  if (newBp != c.bb.Bp) c.bb.flags_init = false;
+  c.bb.Bp = newBp;
+  // the staged values become the batch's field-major values (the in-kernel
+  // recover of ks_solve reads J_d, D_s, r_s, r_yd from there); the slot
+  // takes the previous buffer, free since the previous solve returned
+  std::swap(c.bvals.p, c.stage[sl].p);
+  std::swap(c.bvals.n, c.stage[sl].n);
+  batch_interleave_inputs(c, c.bvals.p);
+  CK(cudaEventRecord(c.stage_free[sl], c.stream));
+  c.stage_free_rec[sl] = true;
+}
+
+// Asynchronous download of the last batched solve's outputs (pinned host
+// memory): a device copy on the solve stream, then the D2H on the copy
+// stream, so the next solve overlaps it.  hykkt_batch_sync waits for it.
+void batch_download_async(Ctx& c, double* dx, double* ds, double* dy, double* dyd) {
+  if (c.batch <= 0) throw StateError("no batch uploaded");
+  ensure_copy_stream(c);
+  const KktPlan& k = c.kp;
+  const idx B = c.batch, nout = k.nx + k.mc + 2 * k.md;
+  c.out_stage.alloc(static_cast<std::size_t>(B * nout));
+  if (c.out_free_rec) CK(cudaStreamWaitEvent(c.stream, c.out_free, 0));
+  CK(cudaMemcpyAsync(c.out_stage.p, c.bouts.p, B * nout * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  CK(cudaEventRecord(c.out_ready, c.stream));
+  CK(cudaStreamWaitEvent(c.copy_stream, c.out_ready, 0));
+  auto dl = [&](const double* srcp, double* out, idx n) {
+    if (out && n) CK(cudaMemcpyAsync(out, srcp, n * sizeof(double), cudaMemcpyDefault, c.copy_stream));
+  };
+  const double* o = c.out_stage.p;
+  dl(o, dx, B * k.nx);
+  dl(o + B * k.nx, dy, B * k.mc);
+  dl(o + B * (k.nx + k.mc), ds, B * k.md);
+  dl(o + B * (k.nx + k.mc + k.md), dyd, B * k.md);
+  CK(cudaEventRecord(c.out_free, c.copy_stream));
+  c.out_free_rec = true;
+}
+
+void batch_sync(Ctx& c) {
+  if (c.copy_stream) CK(cudaStreamSynchronize(c.copy_stream));
+  CK(cudaStreamSynchronize(c.stream));
 }
 
 int pow2_at_least(long long v) {
@@ -1600,7 +1708,7 @@ int pow2_at_least(long long v) {
 }
 
 // Interleaved [entry][system] copies of the uploaded field-major values.
-void batch_interleave_inputs(Ctx& c) {
+void batch_interleave_inputs(Ctx& c, const double* src) {
   auto& bb = c.bb;
   const BatchLayout L = batch_layout(c.kp);
   const int B = static_cast<int>(c.batch), Bp = bb.Bp;
@@ -1613,7 +1721,7 @@ void batch_interleave_inputs(Ctx& c) {
     bb.f[i] = bb.vals.p + off_out * Bp;
     if (n > 0) {
       dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>(Bp / 32));
-      dev::kb_interleave<<<grid, 256, 0, c.stream>>>(c.bvals.p + off_in, bb.f[i], static_cast<int>(n), B, Bp);
+      dev::kb_interleave<<<grid, 256, 0, c.stream>>>(src + off_in, bb.f[i], static_cast<int>(n), B, Bp);
       check_launch(c);
     }
     off_in += n * B;
@@ -1896,6 +2004,7 @@ bool ks_prepare(Ctx& c) {
 // sweeps, the delta1 ladder (solver.cpp:108-142) with a fresh
 // RegularizationState per system, CG stop rules, the delta2 restart.
 void batch_solve_resident(Ctx& c, const hykkt_config_t& cfg, int flags, hykkt_report_t* reports) {
+  batch_take_async(c);
   if (c.batch <= 0) throw StateError("no batch uploaded");
   validate_cfg(cfg);
   const KktPlan& k = c.kp;
@@ -2514,6 +2623,16 @@ int hykkt_create(int device, hykkt_t* out) {
 void hykkt_destroy(hykkt_t h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  if (h->copy_stream) {
+    cudaStreamSynchronize(h->copy_stream);
+    cudaStreamDestroy(h->copy_stream);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(h->stage_ready[i]);
+      cudaEventDestroy(h->stage_free[i]);
+    }
+    cudaEventDestroy(h->out_ready);
+    cudaEventDestroy(h->out_free);
+  }
   if (h->stream) {
     cudaStreamSynchronize(h->stream);
     cudaStreamDestroy(h->stream);
@@ -2992,6 +3111,18 @@ int hykkt_batch_solve_resident(hykkt_t h, const hykkt_config_t* cfg, int flags, 
 
 int hykkt_batch_download(hykkt_t h, double* dx, double* ds, double* dy, double* dyd) {
   return guarded([&] { batch_download(ctx(h), dx, ds, dy, dyd); });
+}
+
+int hykkt_batch_upload_async(hykkt_t h, int64_t batch, const hykkt_values_t* values) {
+  return guarded([&] { batch_upload_async(ctx(h), batch, values); });
+}
+
+int hykkt_batch_download_async(hykkt_t h, double* dx, double* ds, double* dy, double* dyd) {
+  return guarded([&] { batch_download_async(ctx(h), dx, ds, dy, dyd); });
+}
+
+int hykkt_batch_sync(hykkt_t h) {
+  return guarded([&] { batch_sync(ctx(h)); });
 }
 
 int hykkt_batch_solve(hykkt_t h, const hykkt_config_t* cfg, int64_t batch, const hykkt_values_t* values,

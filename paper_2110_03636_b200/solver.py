@@ -568,6 +568,31 @@ class Batch:
         v = _lib.Values(*[dp(a) for a in arrs])
         check(_lib.lib().hykkt_batch_upload(self.dev.h, self.count, C.byref(v)))
 
+    def upload_async(self, values: dict) -> None:
+        """Starts the host-to-device copy of the next batch
+        (hykkt_batch_upload_async); the next solve_resident consumes the
+        oldest pending upload.  The arrays must stay alive (and unchanged)
+        until that solve: they are kept referenced here."""
+        arrs = [values[n] for n in VALUE_FIELDS]
+        for a in arrs:
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise _lib.InvalidMatrixError(-1, "batch values must be C-contiguous float64")
+        self._pending = getattr(self, "_pending", [])[-1:] + [arrs]
+        v = _lib.Values(*[dp(a) for a in arrs])
+        check(_lib.lib().hykkt_batch_upload_async(self.dev.h, arrs[0].shape[0], C.byref(v)))
+        if not self.count:
+            self.count = arrs[0].shape[0]
+
+    def download_async(self, out: dict) -> dict:
+        """Starts the device-to-host copy of the last solve's outputs
+        (hykkt_batch_download_async); `out` is complete after sync()."""
+        check(_lib.lib().hykkt_batch_download_async(self.dev.h, dp(out["dx"]), dp(out["ds"]),
+                                                    dp(out["dy"]), dp(out["dyd"])))
+        return out
+
+    def sync(self) -> None:
+        check(_lib.lib().hykkt_batch_sync(self.dev.h))
+
     def upload_device(self, ptrs: dict, count: int) -> None:
         """Values already in device memory (hykkt_batch_upload_device):
         `ptrs` maps each VALUE_FIELDS name to a device address of a

@@ -322,6 +322,42 @@ def test_reanalysis_between_batched_solves(ref):
     dev.close()
 
 
+# ---- pipelined batch copies (hykkt_batch_upload_async / _download_async) ------
+def test_async_batch_copies_match_synchronous_path():
+    """Three drifted value sets through the pipelined protocol (upload of set
+    k+1 issued before the solve of set k, asynchronous downloads) give the
+    same reports and solutions, bit for bit, as upload / solve / download."""
+    from paper_2110_03636_b200.solver import Batch, stack_values
+    cfg = SolverConfig()
+    base = acopf.batch(120, 5, seed=7)
+    sets = [base] + [[acopf.drift(x, 0.01, 31 * k + i) for i, x in enumerate(base)] for k in (1, 2)]
+    vals = [stack_values(v) for v in sets]
+    dev = Device(0)
+    dev.analyze(base[0])
+    bt = Batch(dev)
+    want = []
+    for v in vals:
+        bt.upload(v)
+        reps = bt.solve_resident(cfg)
+        want.append(([r.cg_iterations for r in reps], {k: a.copy() for k, a in bt.download().items()}))
+    outs = [dict(dx=np.zeros((5, base[0].n_x)), ds=np.zeros((5, base[0].m_d)), dy=np.zeros((5, base[0].m_c)),
+                 dyd=np.zeros((5, base[0].m_d))) for _ in vals]
+    bt.upload_async(vals[0])
+    its = []
+    for k in range(len(vals)):
+        if k + 1 < len(vals):
+            bt.upload_async(vals[k + 1])
+        reps = bt.solve_resident(cfg)
+        its.append([r.cg_iterations for r in reps])
+        bt.download_async(outs[k])
+    bt.sync()
+    for k in range(len(vals)):
+        assert its[k] == want[k][0]
+        for name in ("dx", "ds", "dy", "dyd"):
+            assert np.array_equal(outs[k][name], want[k][1][name]), (k, name)
+    dev.close()
+
+
 # ---- device BE / RR (metrics.cpp:28-240 on the device) ----------------------------
 @pytest.mark.parametrize("nb,gamma", [(120, 1e4), (500, 1e8)])
 def test_device_metrics_match_host_and_reference(ref, nb, gamma, monkeypatch):
