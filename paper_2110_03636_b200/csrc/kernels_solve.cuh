@@ -668,19 +668,45 @@ __global__ void __launch_bounds__(256) k_qform(int nrows_total, const int2* __re
 // same arithmetic in the same order as fwd_task's narrow branch.
 template <int NR, int W>
 __device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
+  // Bottom levels are grid-synchronous: every value read here is complete,
+  // so nothing is polled and the loads of all rows are issued together
+  // (row bounds, then the first two gather indices of every row, then their
+  // values); rows with more gathers finish in a second pass.  Same sums in
+  // the same order as the polling form.
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const int rp = s.rows_ptr[sn];
   const double* P = a.panel + s.off[sn];
+  int gp[NR + 1];
+#pragma unroll
+  for (int q = 0; q <= NR; ++q) gp[q] = q <= nr ? __ldg(s.gat_ptr + rp + q) : 0;
+  double rb[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) rb[q] = q < w ? rhs_at(a, f + q) : 0.0;
+  int i0[NR], i1[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const bool row = q < nr;
+    i0[q] = (row && gp[q] < gp[q + 1]) ? __ldg(s.gat_idx + gp[q]) : -1;
+    i1[q] = (row && gp[q] + 1 < gp[q + 1]) ? __ldg(s.gat_idx + gp[q] + 1) : -1;
+  }
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) {
-    acc[q] = 0.0;
+    const double v0 = i0[q] >= 0 ? ldcg(a.u + i0[q]) : 0.0;
+    const double v1 = i1[q] >= 0 ? ldcg(a.u + i1[q]) : 0.0;
+    double g = 0.0;
+    g += v0;
+    g += v1;
+    acc[q] = g;
+  }
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
     if (q < nr) {
-      double g = 0.0;
-      for (int e = __ldg(s.gat_ptr + rp + q), e1 = __ldg(s.gat_ptr + rp + q + 1); e < e1; ++e)
-        g += load_ready(a.u + __ldg(s.gat_idx + e), a.abort);
-      acc[q] = q < w ? rhs_at(a, f + q) - g : g;
+      for (int e = gp[q] + 2; e < gp[q + 1]; ++e) acc[q] += ldcg(a.u + __ldg(s.gat_idx + e));
+      if (q < W && q < w) acc[q] = rb[q < W ? q : 0] - acc[q];
+    } else {
+      acc[q] = 0.0;
     }
   }
 #pragma unroll
@@ -711,9 +737,13 @@ __device__ __forceinline__ void bwd_thread(const TrsvArgs& a, int sn) {
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const double* P = a.panel + s.off[sn];
   const int* R = s.rows + s.rows_ptr[sn];
+  // grid-synchronous bottom level (see fwd_thread): plain loads, all in flight
   double xb[NR], acc[W];
+  int gr[NR];
 #pragma unroll
-  for (int r = 0; r < NR; ++r) xb[r] = (r >= w && r < nr) ? load_ready(a.x + __ldg(R + r), a.abort) : 0.0;
+  for (int r = 0; r < NR; ++r) gr[r] = (r >= w && r < nr) ? __ldg(R + r) : -1;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) xb[r] = gr[r] >= 0 ? ldcg(a.x + gr[r]) : 0.0;
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     acc[k] = 0.0;
@@ -723,7 +753,7 @@ __device__ __forceinline__ void bwd_thread(const TrsvArgs& a, int sn) {
       for (int r = 0; r < NR; ++r) {
         if (r >= w && r < nr) t = fma(__ldg(P + k * nr + r), xb[r], t);
       }
-      acc[k] = load_ready(a.y + f + k, a.abort) - t;
+      acc[k] = ldcg(a.y + f + k) - t;
     }
   }
 #pragma unroll
@@ -839,7 +869,7 @@ __device__ __forceinline__ void rearm(const TrsvArgs& a) {
   reset_unset(a.u, a.s.u_size);
 }
 
-__global__ void __launch_bounds__(256) k_trsv(TrsvArgs a) {
+__global__ void __launch_bounds__(256, 2) k_trsv(TrsvArgs a) {
   __shared__ TrsvSmem S;
   unsigned long long* ps = (a.pstamp && threadIdx.x == 0) ? a.pstamp + 8 * blockIdx.x : nullptr;
   if (ps) ps[0] = global_ns();
