@@ -121,6 +121,7 @@ struct hykkt_context {
   // single-system triangular-solve task streams (kernels_solve.cuh trsv_pass)
   hykkt::DBuf<int> tr_wid, tr_nar, tr_pos;
   int tr_nwid = 0, tr_nnar = 0, tr_nbot = 0;
+  int tr_call = 0;  // narrow tasks as real calls (trsv_pass<true>), chosen per analysis
   hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
   hykkt::DBuf<unsigned char> tr_bot_wide;
   // asynchronous batch copies (hykkt_batch_upload_async / _download_async):
@@ -356,11 +357,12 @@ void init_ctx(Ctx& c, int device) {
   if (!coop) throw CudaError("device does not support cooperative launch");
   c.coop_factor_blocks = occupancy_blocks(c, (const void*)dev::k_factor);
   c.coop_mf_blocks = occupancy_blocks(c, (const void*)dev::k_mf_factor);
-  c.coop_trsv_blocks = occupancy_blocks(c, (const void*)dev::k_trsv);
+  c.coop_trsv_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_trsv<false>),
+                                occupancy_blocks(c, (const void*)dev::k_trsv<true>));
   {
-    c.cg_fn = (const void*)dev::k_cg<2>;  // 2 CTAs per SM (B200 sweep of 2 / 3 / 4 in round 1)
+    c.cg_fn = (const void*)dev::k_cg<2, false>;  // 2 CTAs per SM (B200 sweep of 2 / 3 / 4 in round 1)
   }
-  c.coop_cg_blocks = occupancy_blocks(c, c.cg_fn);
+  c.coop_cg_blocks = std::min(occupancy_blocks(c, c.cg_fn), occupancy_blocks(c, (const void*)dev::k_cg<2, true>));
   c.coop_ruiz_blocks = std::min(occupancy_blocks(c, (const void*)dev::k_ruiz), 2 * c.num_sms);
   c.coop_bfactor_blocks = occupancy_blocks(c, (const void*)dev::kb_factor, kBatchSmem);
   c.coop_btrsv_blocks = occupancy_blocks(c, (const void*)dev::kb_trsv, kBatchSmem);
@@ -687,6 +689,11 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     // B200 sweep: smaller trees (C1-C3) gain from more CTA tasks (256 entries),
     // the 324k-supernode C4 tree from keeping the 48 wide CTAs to its top (1024)
     long long wide = s.nsup <= 65536 ? 256 : 1024;
+    // trees up to 65536 supernodes (C1-C3): narrow tasks as calls with every
+    // task kind pre-waiting (r02: C1 322 -> 260, C2 392 -> 323, C3 567 -> 544
+    // us / CG iteration); larger trees keep them inlined (C4 1553 vs 1897)
+    c.tr_call = s.nsup <= 65536 ? 1 : 0;
+    if (const char* e = std::getenv("HYKKT_TRSV_CALL")) c.tr_call = std::atoi(e) != 0;
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE")) wide = std::max(1ll, std::atoll(e));
     std::vector<int> pos(std::max<idx>(1, s.nsup));
 
@@ -911,8 +918,10 @@ dev::TrsvArgs trsv_args(Ctx& c) {
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
     nwc = std::min({nwc, c.tr_nwid, std::max(1, c.coop_cg_blocks / 2)});
     ta.nwc = c.tr_nwid > 0 ? nwc : 0;
-    ta.pre_wait = 10;  // general tasks poll one value per dependency first, narrow ones poll their own values
-                       // (r02 A/B on the current kernel: 15 = all pre-wait is 10-14 % slower at C1-C4)
+    // pre-wait bits: 1 fwd narrow, 2 fwd general, 4 bwd narrow, 8 bwd general
+    // (poll one value per dependency before loading); with inlined tasks
+    // only the general kinds pre-wait, with task calls all of them (r02 A/B)
+    ta.pre_wait = c.tr_call ? 15 : 10;
     if (const char* e = std::getenv("HYKKT_TRSV_PREWAIT")) ta.pre_wait = std::atoi(e);
   }
   ta.pos = c.tr_pos.p;
@@ -982,7 +991,8 @@ void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, doub
   ta.rhs.u = u;
   ta.rhs.jval = jval;
   ta.ticket = fresh_tickets(c, 2);
-  coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
+  coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
+              &ta);
 }
 
 dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
@@ -1029,7 +1039,7 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   }
   ensure_qform(c);
   a.tickets = fresh_tickets(c, 2 * (cfg.cg_max_iter + 2));
-  coop_launch(c, c.cg_fn, c.coop_cg_blocks, &a);
+  coop_launch(c, c.tr_call ? (const void*)dev::k_cg<2, true> : c.cg_fn, c.coop_cg_blocks, &a);
   return read_status(c).cg;
 }
 
@@ -3047,7 +3057,8 @@ int hykkt_debug_trsv_phases(hykkt_t h, uint64_t* out, int64_t cap, int64_t* nblk
     ta.rhs.b = c.rhat.p;
     ta.pstamp = st.p;
     ta.ticket = fresh_tickets(c, 2);
-    coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
+    coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
+                &ta);
     read_status(c);
     CK(cudaMemcpy(out, st.p, 8 * c.coop_trsv_blocks * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
@@ -3087,7 +3098,8 @@ int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
     ta.rhs.b = c.rhat.p;
     ta.trace = tr.p;
     ta.ticket = fresh_tickets(c, 2);
-    coop_launch(c, (const void*)dev::k_trsv, c.coop_trsv_blocks, &ta);
+    coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
+                &ta);
     read_status(c);
     CK(cudaMemcpy(out, tr.p, 6 * ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });

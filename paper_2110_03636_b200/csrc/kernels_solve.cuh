@@ -209,7 +209,7 @@ __device__ __forceinline__ void wait_children(const TrsvArgs& a, int sn, int lan
 // y = L_ss^-1 (b - acc), rows below: u_s = acc + L_below y, handed to the
 // parent.  Every static load (gather indices, L, right-hand side) is issued
 // before the first wait, so a tree level costs about one L2 round trip.
-__device__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot, double* sA = nullptr) {
+__device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot, double* sA = nullptr) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const int rp = s.rows_ptr[sn];
@@ -329,7 +329,7 @@ __device__ __forceinline__ void wait_parent(const TrsvArgs& a, int sn, int lane)
   __syncwarp();
 }
 
-__device__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
+__device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
   const double* P = a.panel + s.off[sn];
@@ -794,6 +794,17 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
   }
 }
 
+// The narrow-stream tasks as real calls (trsv_pass<true>): a smaller task
+// loop and separately allocated registers; measured faster on the smaller
+// trees (C1-C3) together with pre-wait on every task kind, slower at C4
+// (hykkt_cuda.cu picks per analysis).
+__device__ __noinline__ void fwd_task_call(const TrsvArgs& a, int sn, int lane, int tslot, double* sA) {
+  fwd_task(a, sn, lane, tslot, sA);
+}
+__device__ __noinline__ void bwd_task_call(const TrsvArgs& a, int sn, int lane, int tslot) {
+  bwd_task(a, sn, lane, tslot);
+}
+
 // One forward + backward pass; y and x must hold kUnset on entry.
 // Two task streams, each in topological order (forward list, then the same
 // list reversed for the backward pass):
@@ -802,6 +813,7 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
 // Both streams follow one global topological order and each is taken in
 // order, so the smallest unfinished task always has its dependencies held by
 // running CTAs / warps: no deadlock.
+template <bool CALL>
 __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int ns = a.s.nsup;
@@ -849,8 +861,13 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
       const int sn = a.nar_sn[fwd ? t : 2 * nt - 1 - t];
       const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
       if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
-      if (fwd) fwd_task(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
-      else bwd_task(a, sn, lane, slot);
+      if (CALL) {
+        if (fwd) fwd_task_call(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+        else bwd_task_call(a, sn, lane, slot);
+      } else {
+        if (fwd) fwd_task(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+        else bwd_task(a, sn, lane, slot);
+      }
       if (a.trace && lane == 0) a.trace[slot] = global_ns();
     }
   }
@@ -869,6 +886,7 @@ __device__ __forceinline__ void rearm(const TrsvArgs& a) {
   reset_unset(a.u, a.s.u_size);
 }
 
+template <bool CALL>
 __global__ void __launch_bounds__(256, 2) k_trsv(TrsvArgs a) {
   __shared__ TrsvSmem S;
   unsigned long long* ps = (a.pstamp && threadIdx.x == 0) ? a.pstamp + 8 * blockIdx.x : nullptr;
@@ -876,7 +894,7 @@ __global__ void __launch_bounds__(256, 2) k_trsv(TrsvArgs a) {
   rearm(a);
   grid_sync(a.bar, a.abort);
   if (ps) ps[1] = global_ns();
-  trsv_pass(a, S);
+  trsv_pass<CALL>(a, S);
   if (ps) ps[7] = global_ns();
 }
 
@@ -943,7 +961,7 @@ __device__ __forceinline__ double reduce_partials(const double* partials, int sl
   return block_sum(v, scratch);
 }
 
-template <int MINB>
+template <int MINB, bool CALL>
 __global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
   __shared__ double scratch[33];
   __shared__ TrsvSmem S;
@@ -974,7 +992,7 @@ __global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
   TrsvArgs tr = a.tr;
   for (long long it = 1; it <= a.max_iter; ++it) {
     tr.ticket = a.tickets + 2 * it;
-    trsv_pass(tr, S);
+    trsv_pass<CALL>(tr, S);
     grid_sync(bar, abort);
     double pq = 0.0, pp = 0.0;
     for (int k = gt; k < a.mc; k += gs) {

@@ -127,6 +127,9 @@ VARIANTS = {
     # opt-in: wide supernodes in Q-form (inverted diagonal block, row /
     # column slices over the wide CTAs), every supernode wide
     "qform": {"HYKKT_QFORM": "1", "HYKKT_TRSV_WIDE": "1", "HYKKT_TRSV_BOTTOM_MIN": "100000000"},
+    # the narrow tasks inlined into the task loop (the default above 65536
+    # supernodes; small trees call them)
+    "inline_tasks": {"HYKKT_TRSV_CALL": "0"},
 }
 
 
