@@ -209,6 +209,7 @@ __device__ __forceinline__ void wait_children(const TrsvArgs& a, int sn, int lan
 // y = L_ss^-1 (b - acc), rows below: u_s = acc + L_below y, handed to the
 // parent.  Every static load (gather indices, L, right-hand side) is issued
 // before the first wait, so a tree level costs about one L2 round trip.
+template <bool MID>
 __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot, double* sA = nullptr) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
@@ -230,6 +231,8 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
 #pragma unroll
     for (int k = 0; k < 4; ++k) lrow[k] = (row && k < w) ? __ldg(P + k * nr + lane) : 0.0;
     const double bi = own ? rhs_at(a, f + lane) : 0.0;
+    // reciprocal of this lane's diagonal entry, off the dependency chain
+    const double rdl = own ? 1.0 / __ldg(P + lane * nr + lane) : 1.0;
     if (a.pre_wait & 1) wait_children(a, sn, lane);
     double xv[4];
 #pragma unroll
@@ -246,7 +249,7 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (k < w) {
-        const double yk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, lrow[k], k);
+        const double yk = __shfl_sync(0xffffffffu, acc * rdl, k);
         if (lane == k) acc = yk;
         if (lane > k && lane < w) acc = fma(-lrow[k], yk, acc);
         if (lane >= w && row) acc = fma(lrow[k], yk, acc);
@@ -254,6 +257,67 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
     }
     if (own) stcg(a.y + f + lane, acc);
     if (lane >= w && row) stcg(U + lane - w, acc);
+    return;
+  }
+  if (MID && nr <= 64 && w <= 16) {
+    // Medium supernode: lane owns rows lane and lane + 32.  The same flow as
+    // the narrow branch -- every static load (gather lists, panel rows,
+    // right-hand side, reciprocal diagonal) before the first wait, the
+    // children's values gathered row-side in child order, then a shuffle
+    // chain -- instead of the general branch's per-child extend-add and
+    // per-chunk panel loads.
+    const int q0 = lane, q1 = lane + 32;
+    const bool own = lane < w, row0 = q0 < nr, row1 = q1 < nr;
+    const int gb0 = row0 ? __ldg(s.gat_ptr + rp + q0) : 0, ge0 = row0 ? __ldg(s.gat_ptr + rp + q0 + 1) : 0;
+    const int gb1 = row1 ? __ldg(s.gat_ptr + rp + q1) : 0, ge1 = row1 ? __ldg(s.gat_ptr + rp + q1 + 1) : 0;
+    int g0[3], g1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      g0[k] = (gb0 + k < ge0) ? __ldg(s.gat_idx + gb0 + k) : -1;
+      g1[k] = (gb1 + k < ge1) ? __ldg(s.gat_idx + gb1 + k) : -1;
+    }
+    double p0[16], p1[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      p0[k] = (row0 && k < w) ? __ldg(P + k * nr + q0) : 0.0;
+      p1[k] = (row1 && k < w) ? __ldg(P + k * nr + q1) : 0.0;
+    }
+    const double bi = own ? rhs_at(a, f + lane) : 0.0;
+    const double rdl = own ? 1.0 / __ldg(P + lane * nr + lane) : 1.0;
+    if (a.pre_wait & 2) wait_children(a, sn, lane);
+    double A0 = 0.0, A1 = 0.0;
+    {
+      double v0[3], v1[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        v0[k] = g0[k] >= 0 ? ldcg(a.u + g0[k]) : 0.0;
+        v1[k] = g1[k] >= 0 ? ldcg(a.u + g1[k]) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (g0[k] >= 0 && __double_as_longlong(v0[k]) == kUnset) v0[k] = poll_value(a.u + g0[k], a.abort);
+        if (g1[k] >= 0 && __double_as_longlong(v1[k]) == kUnset) v1[k] = poll_value(a.u + g1[k], a.abort);
+        A0 += v0[k];
+        A1 += v1[k];
+      }
+      if (ge0 - gb0 > 3) A0 += gather_u(a, gb0 + 3, ge0);
+      if (ge1 - gb1 > 3) A1 += gather_u(a, gb1 + 3, ge1);
+    }
+    if (own) A0 = bi - A0;
+    if (a.trace) { __syncwarp(); if (lane == 0) a.trace[4 * a.s.nsup + tslot] = global_ns(); }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < w) {
+        const double yk = __shfl_sync(0xffffffffu, A0 * rdl, k);
+        if (lane == k) A0 = yk;
+        if (lane > k && lane < w) A0 = fma(-p0[k], yk, A0);
+        if (lane >= w && row0) A0 = fma(p0[k], yk, A0);
+        if (row1) A1 = fma(p1[k], yk, A1);
+      }
+    }
+    if (own) stcg(a.y + f + lane, A0);
+    else if (row0) stcg(U + q0 - w, A0);
+    if (row1) stcg(U + q1 - w, A1);
     return;
   }
   // General supernode: A[q] (per-supernode scratch) holds, for own rows,
@@ -294,11 +358,12 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
     double d[32];  // row cb+lane of the chunk's diagonal block, all loads in flight
 #pragma unroll
     for (int k = 0; k < 32; ++k) d[k] = (k < cw && lane < cw) ? __ldg(P + (cb + k) * nr + cb + lane) : 0.0;
+    const double rdl = lane < cw ? 1.0 / __ldg(P + (cb + lane) * nr + cb + lane) : 1.0;
     double acc = lane < cw ? A[cb + lane] : 0.0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       if (k < cw) {
-        const double yk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, d[k], k);
+        const double yk = __shfl_sync(0xffffffffu, acc * rdl, k);
         if (lane == k) acc = yk;
         if (lane > k && lane < cw) acc = fma(-d[k], yk, acc);
       }
@@ -329,6 +394,7 @@ __device__ __forceinline__ void wait_parent(const TrsvArgs& a, int sn, int lane)
   __syncwarp();
 }
 
+template <bool MID>
 __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
@@ -344,6 +410,7 @@ __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, in
     for (int k = 0; k < 4; ++k) lv[k] = (lane < below && k < w) ? __ldg(P + k * nr + w + lane) : 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) ld[k] = (lane < w && k < w) ? __ldg(P + lane * nr + k) : 0.0;  // L(k, lane)
+    const double rdl = lane < w ? 1.0 / __ldg(P + lane * nr + lane) : 1.0;
     if (a.pre_wait & 4) wait_parent(a, sn, lane);
     double acc = lane < w ? load_ready(a.y + f + lane, a.abort) : 0.0;
     const double xr = lane < below ? load_ready(a.x + gr, a.abort) : 0.0;
@@ -358,7 +425,47 @@ __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, in
 #pragma unroll
     for (int k = 3; k >= 0; --k) {
       if (k < w) {
-        const double xk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, ld[k], k);
+        const double xk = __shfl_sync(0xffffffffu, acc * rdl, k);
+        if (lane == k) acc = xk;
+        if (lane < k) acc = fma(-ld[k], xk, acc);
+      }
+    }
+    if (lane < w) {
+      stcg(a.x + f + lane, acc);
+      if (a.x_out) a.x_out[s.perm[f + lane]] = acc;
+    }
+    return;
+  }
+  if (MID && w <= 16 && nr - w <= 64) {
+    // Medium supernode: lanes hold the rows below (two each, x gathered
+    // once), column sums by warp reductions, then the diagonal block's chain
+    // with lane = column; all static loads before the wait.
+    const int below = nr - w, r0 = lane, r1 = lane + 32;
+    const int gr0 = r0 < below ? __ldg(R + w + r0) : 0, gr1 = r1 < below ? __ldg(R + w + r1) : 0;
+    double l0[16], l1[16], ld[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      l0[k] = (r0 < below && k < w) ? __ldg(P + k * nr + w + r0) : 0.0;
+      l1[k] = (r1 < below && k < w) ? __ldg(P + k * nr + w + r1) : 0.0;
+      ld[k] = (lane < w && k < w) ? __ldg(P + lane * nr + k) : 0.0;  // L(k, lane)
+    }
+    const double rdl = lane < w ? 1.0 / __ldg(P + lane * nr + lane) : 1.0;
+    if (a.pre_wait & 8) wait_parent(a, sn, lane);
+    double acc = lane < w ? load_ready(a.y + f + lane, a.abort) : 0.0;
+    const double x0 = r0 < below ? load_ready(a.x + gr0, a.abort) : 0.0;
+    const double x1 = r1 < below ? load_ready(a.x + gr1, a.abort) : 0.0;
+    if (a.trace) { __syncwarp(); if (lane == 0) a.trace[4 * a.s.nsup + tslot] = global_ns(); }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < w) {
+        const double t = warp_sum(fma(l1[k], x1, l0[k] * x0));
+        if (lane == k) acc -= t;
+      }
+    }
+#pragma unroll
+    for (int k = 15; k >= 0; --k) {
+      if (k < w) {
+        const double xk = __shfl_sync(0xffffffffu, acc * rdl, k);
         if (lane == k) acc = xk;
         if (lane < k) acc = fma(-ld[k], xk, acc);
       }
@@ -375,6 +482,7 @@ __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, in
     double d[32];  // column cb+lane of the chunk's diagonal block: L(cb+k, cb+lane)
 #pragma unroll
     for (int k = 0; k < 32; ++k) d[k] = (k < cw && lane < cw) ? __ldg(P + (cb + lane) * nr + cb + k) : 0.0;
+    const double rdl = lane < cw ? 1.0 / __ldg(P + (cb + lane) * nr + cb + lane) : 1.0;
     if (ci == nchunks - 1 && (a.pre_wait & 8)) wait_parent(a, sn, lane);
     double acc = lane < cw ? load_ready(a.y + f + cb + lane, a.abort) : 0.0;
     const int rb0 = cb + cw;  // rows below this chunk (own later chunks + ancestors)
@@ -392,7 +500,7 @@ __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, in
 #pragma unroll
     for (int k = 31; k >= 0; --k) {
       if (k < cw) {
-        const double xk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, d[k], k);
+        const double xk = __shfl_sync(0xffffffffu, acc * rdl, k);
         if (lane == k) acc = xk;
         if (lane < k) acc = fma(-d[k], xk, acc);
       }
@@ -709,10 +817,13 @@ __device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
       acc[q] = 0.0;
     }
   }
+  double rd[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) rd[k] = k < w ? 1.0 / __ldg(P + k * nr + k) : 1.0;
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     if (k < w) {
-      const double yk = acc[k] / __ldg(P + k * nr + k);
+      const double yk = acc[k] * rd[k];
       acc[k] = yk;
 #pragma unroll
       for (int q = k + 1; q < NR; ++q) {
@@ -756,10 +867,13 @@ __device__ __forceinline__ void bwd_thread(const TrsvArgs& a, int sn) {
       acc[k] = ldcg(a.y + f + k) - t;
     }
   }
+  double rd[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) rd[k] = k < w ? 1.0 / __ldg(P + k * nr + k) : 1.0;
 #pragma unroll
   for (int k = W - 1; k >= 0; --k) {
     if (k < w) {
-      const double xk = acc[k] / __ldg(P + k * nr + k);
+      const double xk = acc[k] * rd[k];
       acc[k] = xk;
 #pragma unroll
       for (int j = 0; j < k; ++j) acc[j] = fma(-__ldg(P + j * nr + k), xk, acc[j]);
@@ -795,14 +909,15 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
 }
 
 // The narrow-stream tasks as real calls (trsv_pass<true>): a smaller task
-// loop and separately allocated registers; measured faster on the smaller
-// trees (C1-C3) together with pre-wait on every task kind, slower at C4
-// (hykkt_cuda.cu picks per analysis).
+// loop, separately allocated registers and the medium (w <= 16) branches;
+// measured faster on the smaller trees (C1-C3) together with pre-wait on
+// every task kind, slower at C4 (hykkt_cuda.cu picks per analysis;
+// DESIGN.md §10).
 __device__ __noinline__ void fwd_task_call(const TrsvArgs& a, int sn, int lane, int tslot, double* sA) {
-  fwd_task(a, sn, lane, tslot, sA);
+  fwd_task<true>(a, sn, lane, tslot, sA);
 }
 __device__ __noinline__ void bwd_task_call(const TrsvArgs& a, int sn, int lane, int tslot) {
-  bwd_task(a, sn, lane, tslot);
+  bwd_task<true>(a, sn, lane, tslot);
 }
 
 // One forward + backward pass; y and x must hold kUnset on entry.
@@ -865,8 +980,8 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
         if (fwd) fwd_task_call(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
         else bwd_task_call(a, sn, lane, slot);
       } else {
-        if (fwd) fwd_task(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
-        else bwd_task(a, sn, lane, slot);
+        if (fwd) fwd_task<false>(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+        else bwd_task<false>(a, sn, lane, slot);
       }
       if (a.trace && lane == 0) a.trace[slot] = global_ns();
     }
