@@ -744,8 +744,10 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     // substitution tasks)
     c.q_nrows = c.q_nsf = c.q_nsb = 0;
     {
+      // default on for trees above 65536 supernodes (C4: 1491 -> 1430 us per
+      // CG iteration with 96 wide CTAs, r02); the smaller trees are neutral
       const char* e = std::getenv("HYKKT_QFORM");
-      bool on = e ? std::atoi(e) != 0 : false;
+      bool on = e ? std::atoi(e) != 0 : s.nsup > 65536;
       for (int sn : wid)
         if (s.sn_first[sn + 1] - s.sn_first[sn] > dev::kQMaxW) on = false;
       if (on && !wid.empty()) {
@@ -914,7 +916,7 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.nnar = c.tr_nnar;
   {
     // CTAs reserved for the wide stream (B200 sweep at C2-C4: 48 of 296)
-    int nwc = 48;
+    int nwc = c.q_nsf > 0 ? 96 : 48;  // Q-form slices are independent: more CTAs pay (r02)
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
     nwc = std::min({nwc, c.tr_nwid, std::max(1, c.coop_cg_blocks / 2)});
     ta.nwc = c.tr_nwid > 0 ? nwc : 0;
