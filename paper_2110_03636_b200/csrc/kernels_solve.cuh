@@ -133,6 +133,10 @@ struct TrsvArgs {
   int nqb;
 };
 
+#ifndef HYKKT_INLINE_MID
+#define HYKKT_INLINE_MID 0  // 8 measured 1450 vs 1428 us per CG iteration at C4 (r02)
+#endif
+constexpr int kInlineMid = HYKKT_INLINE_MID;  // medium branch width cap of the inlined task loop (0 = off)
 constexpr int kWideMaxRows = 2048;  // wide (CTA) solve tasks stage nrows doubles in shared memory
 constexpr int kWarpRows = kWideMaxRows / 8;  // narrow-task CTAs: each warp's slice of the same buffer
 struct TrsvSmem {
@@ -209,7 +213,7 @@ __device__ __forceinline__ void wait_children(const TrsvArgs& a, int sn, int lan
 // y = L_ss^-1 (b - acc), rows below: u_s = acc + L_below y, handed to the
 // parent.  Every static load (gather indices, L, right-hand side) is issued
 // before the first wait, so a tree level costs about one L2 round trip.
-template <bool MID>
+template <int MID>
 __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, int tslot, double* sA = nullptr) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
@@ -259,7 +263,7 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
     if (lane >= w && row) stcg(U + lane - w, acc);
     return;
   }
-  if (MID && nr <= 64 && w <= 16) {
+  if (MID > 0 && nr <= 64 && w <= MID) {
     // Medium supernode: lane owns rows lane and lane + 32.  The same flow as
     // the narrow branch -- every static load (gather lists, panel rows,
     // right-hand side, reciprocal diagonal) before the first wait, the
@@ -276,9 +280,10 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
       g0[k] = (gb0 + k < ge0) ? __ldg(s.gat_idx + gb0 + k) : -1;
       g1[k] = (gb1 + k < ge1) ? __ldg(s.gat_idx + gb1 + k) : -1;
     }
-    double p0[16], p1[16];
+    constexpr int MW = MID > 0 ? MID : 1;
+    double p0[MW], p1[MW];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < MW; ++k) {
       p0[k] = (row0 && k < w) ? __ldg(P + k * nr + q0) : 0.0;
       p1[k] = (row1 && k < w) ? __ldg(P + k * nr + q1) : 0.0;
     }
@@ -306,7 +311,7 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
     if (own) A0 = bi - A0;
     if (a.trace) { __syncwarp(); if (lane == 0) a.trace[4 * a.s.nsup + tslot] = global_ns(); }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < MW; ++k) {
       if (k < w) {
         const double yk = __shfl_sync(0xffffffffu, A0 * rdl, k);
         if (lane == k) A0 = yk;
@@ -394,7 +399,7 @@ __device__ __forceinline__ void wait_parent(const TrsvArgs& a, int sn, int lane)
   __syncwarp();
 }
 
-template <bool MID>
+template <int MID>
 __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, int tslot) {
   const SnPlan& s = a.s;
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn];
@@ -436,15 +441,16 @@ __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, in
     }
     return;
   }
-  if (MID && w <= 16 && nr - w <= 64) {
+  if (MID > 0 && w <= MID && nr - w <= 64) {
     // Medium supernode: lanes hold the rows below (two each, x gathered
     // once), column sums by warp reductions, then the diagonal block's chain
     // with lane = column; all static loads before the wait.
     const int below = nr - w, r0 = lane, r1 = lane + 32;
     const int gr0 = r0 < below ? __ldg(R + w + r0) : 0, gr1 = r1 < below ? __ldg(R + w + r1) : 0;
-    double l0[16], l1[16], ld[16];
+    constexpr int MW = MID > 0 ? MID : 1;
+    double l0[MW], l1[MW], ld[MW];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < MW; ++k) {
       l0[k] = (r0 < below && k < w) ? __ldg(P + k * nr + w + r0) : 0.0;
       l1[k] = (r1 < below && k < w) ? __ldg(P + k * nr + w + r1) : 0.0;
       ld[k] = (lane < w && k < w) ? __ldg(P + lane * nr + k) : 0.0;  // L(k, lane)
@@ -456,14 +462,14 @@ __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, in
     const double x1 = r1 < below ? load_ready(a.x + gr1, a.abort) : 0.0;
     if (a.trace) { __syncwarp(); if (lane == 0) a.trace[4 * a.s.nsup + tslot] = global_ns(); }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < MW; ++k) {
       if (k < w) {
         const double t = warp_sum(fma(l1[k], x1, l0[k] * x0));
         if (lane == k) acc -= t;
       }
     }
 #pragma unroll
-    for (int k = 15; k >= 0; --k) {
+    for (int k = MW - 1; k >= 0; --k) {
       if (k < w) {
         const double xk = __shfl_sync(0xffffffffu, acc * rdl, k);
         if (lane == k) acc = xk;
@@ -914,10 +920,10 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
 // every task kind, slower at C4 (hykkt_cuda.cu picks per analysis;
 // DESIGN.md §10).
 __device__ __noinline__ void fwd_task_call(const TrsvArgs& a, int sn, int lane, int tslot, double* sA) {
-  fwd_task<true>(a, sn, lane, tslot, sA);
+  fwd_task<16>(a, sn, lane, tslot, sA);
 }
 __device__ __noinline__ void bwd_task_call(const TrsvArgs& a, int sn, int lane, int tslot) {
-  bwd_task<true>(a, sn, lane, tslot);
+  bwd_task<16>(a, sn, lane, tslot);
 }
 
 // One forward + backward pass; y and x must hold kUnset on entry.
@@ -980,8 +986,8 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
         if (fwd) fwd_task_call(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
         else bwd_task_call(a, sn, lane, slot);
       } else {
-        if (fwd) fwd_task<false>(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
-        else bwd_task<false>(a, sn, lane, slot);
+        if (fwd) fwd_task<kInlineMid>(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+        else bwd_task<kInlineMid>(a, sn, lane, slot);
       }
       if (a.trace && lane == 0) a.trace[slot] = global_ns();
     }
