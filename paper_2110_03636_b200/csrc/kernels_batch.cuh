@@ -424,6 +424,7 @@ __device__ void bfactor_task(const BFactorArgs& a, int sn, int tile, int lane) {
         atomicMin(a.fail_col + b, f + k);
       }
       const double dk = sqrt(pivot);
+      const double rdk = 1.0 / dk;  // one division per column, the scaling multiplies
       Pk[(long long)k * Bp] = dk;
       for (int r0 = k + 1; r0 < nr; r0 += kIlp) {
         double v[kIlp];
@@ -431,7 +432,7 @@ __device__ void bfactor_task(const BFactorArgs& a, int sn, int tile, int lane) {
         for (int t = 0; t < kIlp; ++t) v[t] = r0 + t < nr ? Pk[(long long)(r0 + t) * Bp] : 0.0;
 #pragma unroll
         for (int t = 0; t < kIlp; ++t) {
-          if (r0 + t < nr) Pk[(long long)(r0 + t) * Bp] = v[t] / dk;
+          if (r0 + t < nr) Pk[(long long)(r0 + t) * Bp] = v[t] * rdk;
         }
       }
       for (int c = k + 1; c < w; ++c) {
@@ -573,10 +574,10 @@ __device__ void wfactor_task(const BFactorArgs& a, int sn, int b, double* sm) {
             failed = true;
             if (lane == 0) atomicMin(a.fail_col + b, f + k);
           }
-          const double dk = sqrt(pivot);
+          const double dk = sqrt(pivot), rdk = 1.0 / dk;
           __syncwarp();
           if (lane == 0) Pk[k] = dk;
-          for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] / dk;
+          for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] * rdk;
           __syncwarp();
           for (int c = k + 1; c < k0 + kb; ++c) {
             const double lck = Pk[c];

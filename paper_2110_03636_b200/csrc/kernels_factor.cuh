@@ -122,8 +122,8 @@ __device__ void factor_task(const FactorArgs& a, int sn, int lane, double floor_
         if (lane == 0) atomicMin(a.fail_col, f + k);
         break;
       }
-      const double dk = sqrt(pivot);
-      for (int r = k + 1 + lane; r < nr; r += 32) stcg(Pk + r, ldcg(Pk + r) / dk);
+      const double dk = sqrt(pivot), rdk = 1.0 / dk;
+      for (int r = k + 1 + lane; r < nr; r += 32) stcg(Pk + r, ldcg(Pk + r) * rdk);
       __syncwarp();
       if (lane == 0) stcg(Pk + k, dk);
       for (int c = k + 1; c < w; ++c) {

@@ -208,8 +208,8 @@ __device__ void mf_warp_task(const MfArgs& a, int sn, int lane, double floor_v) 
         failed = true;
         break;
       }
-      const double dk = sqrt(pivot);
-      for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = ldcg(Pk + r) / dk;
+      const double dk = sqrt(pivot), rdk = 1.0 / dk;  // one division per column
+      for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = ldcg(Pk + r) * rdk;
       __syncwarp();
       if (lane == 0) Pk[k] = dk;
       for (int c = k + 1; c < w; ++c) {
@@ -276,9 +276,9 @@ __device__ void mf_cta_task(const MfArgs& a, MfSmem& S, int sn, double floor_v) 
             fail = k;
             break;
           }
-          const double dk = sqrt(piv);
+          const double dk = sqrt(piv), rdk = 1.0 / dk;
           __syncwarp();
-          if (lane > k) S.d[k][lane] /= dk;
+          if (lane > k) S.d[k][lane] *= rdk;
           __syncwarp();
           if (lane == k) S.d[k][k] = dk;  // the row's owner: no cross-lane hazard
           const double lrk = S.d[k][lane];

@@ -912,7 +912,7 @@ __device__ __forceinline__ void kf_dense_warp(double* P, int nr, int w, int f, d
     if (!(pivot > floor_v) && lane == 0) atomicMin(fail, f + k);
     const double dk = sqrt(pivot);
     __syncwarp();
-    for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] / dk;
+    for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] * (1.0 / dk);
     if (lane == 0) Pk[k] = dk;
     __syncwarp();
     for (int c = k + 1; c < w; ++c) {
@@ -1113,7 +1113,7 @@ __device__ void kf_cta_task(const KfArgs& a, double* Pb, int sn, double floor_v,
         if (!(pivot > floor_v) && lane == 0) atomicMin(fail, f + k);
         const double dk = sqrt(pivot);
         __syncwarp();
-        for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] / dk;
+        for (int r = k + 1 + lane; r < nr; r += 32) Pk[r] = Pk[r] * (1.0 / dk);
         if (lane == 0) Pk[k] = dk;
         __syncwarp();
         for (int c = k + 1; c < k0 + kb; ++c) {
