@@ -119,7 +119,7 @@ struct hykkt_context {
   hykkt::DBuf<double> mf_ubuf;
   int mf_ntasks = 0, mf_on = 1;
   // single-system triangular-solve task streams (kernels_solve.cuh trsv_pass)
-  hykkt::DBuf<int> tr_wid, tr_nar, tr_pos;
+  hykkt::DBuf<int> tr_wid, tr_nar, tr_nar_bwd, tr_pos, tr_chain_ptr, tr_chain_sn;
   int tr_nwid = 0, tr_nnar = 0, tr_nbot = 0;
   int tr_call = 0;  // narrow tasks as real calls (trsv_pass<true>), chosen per analysis
   hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
@@ -776,6 +776,61 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
         c.q_ver = -1;
       }
     }
+    // chains: a narrow supernode (w <= 4, rows <= 32) whose parent is a
+    // narrow supernode with no other child continues into it; each maximal
+    // chain becomes one narrow-stream entry, at its lowest member's position
+    // forward and its top member's position backward, solved by one warp.
+    // Default with the inlined tasks (C4: 1445 -> 1392 us per CG iteration);
+    // with task calls (C1-C3) a chain link costs as much as a hand-off
+    // (each member's static loads follow the previous member) and the
+    // chains measured slower (r02: C2 285 -> 351).  HYKKT_TRSV_CHAINS=0/1.
+    std::vector<int> chain_ptr{0}, chain_sn, nar_bwd;
+    {
+      const char* e = std::getenv("HYKKT_TRSV_CHAINS");
+      const bool on = e ? std::atoi(e) != 0 : !c.tr_call;
+      std::vector<char> is_nar(s.nsup, 0), link_up(s.nsup, 0), linked_from_below(s.nsup, 0);
+      auto small = [&](int sn) {
+        return s.sn_first[sn + 1] - s.sn_first[sn] <= 4 && s.sn_nrows[sn] <= 32;
+      };
+      for (int sn : nar) is_nar[sn] = 1;
+      if (on) {
+        for (int sn : nar) {
+          const int p = s.sn_parent[sn];
+          if (p >= 0 && is_nar[p] && small(sn) && small(p) && s.child_ptr[p + 1] - s.child_ptr[p] == 1) {
+            link_up[sn] = 1;
+            linked_from_below[p] = 1;
+          }
+        }
+      }
+      std::vector<int> out, top_of(s.nsup, -1);
+      out.reserve(nar.size());
+      for (int sn : nar) {
+        if (linked_from_below[sn]) continue;  // emitted with the chain below it
+        if (!link_up[sn]) {
+          out.push_back(sn);
+          continue;
+        }
+        const int k = static_cast<int>(chain_ptr.size()) - 1;
+        int x = sn;
+        for (;; x = s.sn_parent[x]) {
+          chain_sn.push_back(x);
+          if (!link_up[x]) break;
+        }
+        top_of[x] = k;
+        chain_ptr.push_back(static_cast<int>(chain_sn.size()));
+        out.push_back(-k - 1);
+      }
+      // backward order: reverse topological, each chain at its top member
+      for (auto it = nar.rbegin(); it != nar.rend(); ++it) {
+        const int sn = *it;
+        if (top_of[sn] >= 0) nar_bwd.push_back(-top_of[sn] - 1);
+        else if (!link_up[sn] && !linked_from_below[sn]) nar_bwd.push_back(sn);
+      }
+      nar.swap(out);
+    }
+    c.tr_nar_bwd.upload(nar_bwd.empty() ? std::vector<int>{0} : nar_bwd, st);
+    c.tr_chain_ptr.upload(chain_ptr, st);
+    c.tr_chain_sn.upload(chain_sn.empty() ? std::vector<int>{0} : chain_sn, st);
     c.tr_wid.upload(wid.empty() ? std::vector<int>{0} : wid, st);
     c.tr_nar.upload(nar.empty() ? std::vector<int>{0} : nar, st);
     c.tr_nwid = static_cast<int>(wid.size());
@@ -914,6 +969,9 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.nwid = c.tr_nwid;
   ta.nar_sn = c.tr_nar.p;
   ta.nnar = c.tr_nnar;
+  ta.nar_bwd = c.tr_nar_bwd.p;
+  ta.chain_ptr = c.tr_chain_ptr.p;
+  ta.chain_sn = c.tr_chain_sn.p;
   {
     // CTAs reserved for the wide stream (B200 sweep at C2-C4: 48 of 296)
     int nwc = c.q_nsf > 0 ? 96 : 48;  // Q-form slices are independent: more CTAs pay (r02)

@@ -131,6 +131,11 @@ struct TrsvArgs {
   int nqf;
   const int4* qs_b;
   int nqb;
+  // chains of the narrow stream (nar_sn entries < 0): chain k's supernodes
+  // bottom-up in chain_sn[chain_ptr[k] .. chain_ptr[k+1])
+  const int* chain_ptr;
+  const int* chain_sn;
+  const int* nar_bwd;  // backward order of the narrow stream (chains at their top member)
 };
 
 #ifndef HYKKT_INLINE_MID
@@ -979,17 +984,25 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
     const int nt = a.nnar;
     for (long long t = grab_task(a.ticket + 1, lane); t < 2 * nt; t = grab_task(a.ticket + 1, lane)) {
       const bool fwd = t < nt;
-      const int sn = a.nar_sn[fwd ? t : 2 * nt - 1 - t];
-      const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
-      if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
-      if (CALL) {
-        if (fwd) fwd_task_call(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
-        else bwd_task_call(a, sn, lane, slot);
-      } else {
-        if (fwd) fwd_task<kInlineMid>(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
-        else bwd_task<kInlineMid>(a, sn, lane, slot);
+      const int e = fwd ? a.nar_sn[t] : a.nar_bwd[t - nt];
+      // e >= 0: one supernode; e < 0: chain -e - 1 of single-child narrow
+      // supernodes, solved in order by this warp (forward bottom-up,
+      // backward top-down) with no hand-off to another warp in between
+      const int c0 = e >= 0 ? 0 : a.chain_ptr[-e - 1], cn = e >= 0 ? 1 : a.chain_ptr[-e] - c0;
+      for (int ci = 0; ci < cn; ++ci) {
+        const int sn = e >= 0 ? e : a.chain_sn[c0 + (fwd ? ci : cn - 1 - ci)];
+        const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
+        if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
+        if (CALL) {
+          if (fwd) fwd_task_call(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+          else bwd_task_call(a, sn, lane, slot);
+        } else {
+          if (fwd) fwd_task<kInlineMid>(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+          else bwd_task<kInlineMid>(a, sn, lane, slot);
+        }
+        if (a.trace && lane == 0) a.trace[slot] = global_ns();
+        __syncwarp();
       }
-      if (a.trace && lane == 0) a.trace[slot] = global_ns();
     }
   }
   if (ps) ps[3] = global_ns();

@@ -130,6 +130,10 @@ VARIANTS = {
     # the narrow tasks inlined into the task loop (the default above 65536
     # supernodes; small trees call them)
     "inline_tasks": {"HYKKT_TRSV_CALL": "0"},
+    # single-child chains of narrow supernodes solved by one warp (on by
+    # default with the inlined tasks, forced here with task calls too)
+    "chains_call": {"HYKKT_TRSV_CHAINS": "1"},
+    "no_chains_inline": {"HYKKT_TRSV_CALL": "0", "HYKKT_TRSV_CHAINS": "0"},
 }
 
 
