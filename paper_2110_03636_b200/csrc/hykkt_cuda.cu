@@ -119,7 +119,8 @@ struct hykkt_context {
   hykkt::DBuf<double> mf_ubuf;
   int mf_ntasks = 0, mf_on = 1;
   // single-system triangular-solve task streams (kernels_solve.cuh trsv_pass)
-  hykkt::DBuf<int> tr_wid, tr_nar, tr_nar_bwd, tr_pos, tr_chain_ptr, tr_chain_sn;
+  hykkt::DBuf<int> tr_wid, tr_nar, tr_nar_bwd, tr_pos, tr_chain_ptr, tr_chain_sn, tr_chain_fsrc, tr_chain_bsrc;
+  int tr_chain_regs = 0;
   int tr_nwid = 0, tr_nnar = 0, tr_nbot = 0;
   int tr_call = 0;  // narrow tasks as real calls (trsv_pass<true>), chosen per analysis
   hykkt::DBuf<int> tr_bot_ptr, tr_bot_sn;
@@ -780,14 +781,16 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     // narrow supernode with no other child continues into it; each maximal
     // chain becomes one narrow-stream entry, at its lowest member's position
     // forward and its top member's position backward, solved by one warp.
-    // Default with the inlined tasks (C4: 1445 -> 1392 us per CG iteration);
-    // with task calls (C1-C3) a chain link costs as much as a hand-off
-    // (each member's static loads follow the previous member) and the
-    // chains measured slower (r02: C2 285 -> 351).  HYKKT_TRSV_CHAINS=0/1.
+    // With the inlined tasks (C4) the members run one after the other
+    // through the ordinary task code (1445 -> 1392 us per CG iteration);
+    // with task calls (C1-C3) the chain kernels hand values over in
+    // registers and prefetch each member's static data (chain_fwd /
+    // chain_bwd: C3 530 -> 501; without the hand-off chains were slower,
+    // C2 285 -> 351).  HYKKT_TRSV_CHAINS=0/1, HYKKT_TRSV_CHAIN_REGS=0/1.
     std::vector<int> chain_ptr{0}, chain_sn, nar_bwd;
     {
       const char* e = std::getenv("HYKKT_TRSV_CHAINS");
-      const bool on = e ? std::atoi(e) != 0 : !c.tr_call;
+      const bool on = e ? std::atoi(e) != 0 : true;
       std::vector<char> is_nar(s.nsup, 0), link_up(s.nsup, 0), linked_from_below(s.nsup, 0);
       auto small = [&](int sn) {
         return s.sn_first[sn + 1] - s.sn_first[sn] <= 4 && s.sn_nrows[sn] <= 32;
@@ -810,15 +813,23 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
           out.push_back(sn);
           continue;
         }
-        const int k = static_cast<int>(chain_ptr.size()) - 1;
+        // split into chains of at most 32 members (one lane per member)
         int x = sn;
-        for (;; x = s.sn_parent[x]) {
-          chain_sn.push_back(x);
-          if (!link_up[x]) break;
+        for (;;) {
+          const int k = static_cast<int>(chain_ptr.size()) - 1;
+          int len = 0, top = x;
+          for (;; x = s.sn_parent[x]) {
+            chain_sn.push_back(x);
+            top = x;
+            ++len;
+            if (!link_up[x] || len == 32) break;
+          }
+          top_of[top] = k;
+          chain_ptr.push_back(static_cast<int>(chain_sn.size()));
+          out.push_back(-k - 1);
+          if (!link_up[top]) break;
+          x = s.sn_parent[top];  // the next piece starts above this one
         }
-        top_of[x] = k;
-        chain_ptr.push_back(static_cast<int>(chain_sn.size()));
-        out.push_back(-k - 1);
       }
       // backward order: reverse topological, each chain at its top member
       for (auto it = nar.rbegin(); it != nar.rend(); ++it) {
@@ -829,6 +840,44 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
       nar.swap(out);
     }
     c.tr_nar_bwd.upload(nar_bwd.empty() ? std::vector<int>{0} : nar_bwd, st);
+    // register hand-off tables (kernels_solve.cuh chain_fwd / chain_bwd)
+    {
+      const int nslot = s.sn_rows_ptr.back();
+      std::vector<int> fsrc(std::max(1, nslot), -1), bsrc(std::max(1, nslot), -1);
+      for (std::size_t k = 0; k + 1 < chain_ptr.size(); ++k) {
+        for (int i = chain_ptr[k]; i < chain_ptr[k + 1]; ++i) {
+          const int sn = chain_sn[i], rp = s.sn_rows_ptr[sn], w = s.sn_first[sn + 1] - s.sn_first[sn];
+          const int nr = s.sn_nrows[sn];
+          if (i > chain_ptr[k]) {  // forward: from the member below
+            const int c2 = chain_sn[i - 1], wc = s.sn_first[c2 + 1] - s.sn_first[c2];
+            for (int q = 0; q < nr; ++q) {
+              const int e0 = s.gat_ptr[rp + q], e1 = s.gat_ptr[rp + q + 1];
+              if (e1 - e0 > 1) throw std::logic_error("chain member row with more than one gather");
+              if (e1 > e0) fsrc[rp + q] = wc + (s.gat_idx[e0] - s.u_off[c2]);
+            }
+          }
+          if (i + 1 < chain_ptr[k + 1]) {  // backward: from the member above
+            const int p = chain_sn[i + 1], fp = s.sn_first[p], wp = s.sn_first[p + 1] - fp;
+            const int* Rp = s.sn_rows.data() + s.sn_rows_ptr[p];
+            const int nrp = s.sn_nrows[p];
+            for (int q = w; q < nr; ++q) {
+              const int col = s.sn_rows[rp + q];
+              if (col >= fp && col < fp + wp) {
+                bsrc[rp + q] = col - fp;
+              } else {
+                const int pos = static_cast<int>(std::lower_bound(Rp + wp, Rp + nrp, col) - Rp);
+                if (pos >= nrp || Rp[pos] != col) throw std::logic_error("chain member row outside its parent");
+                bsrc[rp + q] = (pos - wp) | (1 << 8);
+              }
+            }
+          }
+        }
+      }
+      const char* e = std::getenv("HYKKT_TRSV_CHAIN_REGS");
+      c.tr_chain_regs = chain_sn.empty() ? 0 : (e ? std::atoi(e) != 0 : 1);
+      c.tr_chain_fsrc.upload(fsrc, st);
+      c.tr_chain_bsrc.upload(bsrc, st);
+    }
     c.tr_chain_ptr.upload(chain_ptr, st);
     c.tr_chain_sn.upload(chain_sn.empty() ? std::vector<int>{0} : chain_sn, st);
     c.tr_wid.upload(wid.empty() ? std::vector<int>{0} : wid, st);
@@ -971,6 +1020,8 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.nnar = c.tr_nnar;
   ta.nar_bwd = c.tr_nar_bwd.p;
   ta.chain_ptr = c.tr_chain_ptr.p;
+  ta.chain_fsrc = c.tr_chain_regs ? c.tr_chain_fsrc.p : nullptr;
+  ta.chain_bsrc = c.tr_chain_bsrc.p;
   ta.chain_sn = c.tr_chain_sn.p;
   {
     // CTAs reserved for the wide stream (B200 sweep at C2-C4: 48 of 296)
@@ -3099,6 +3150,19 @@ int hykkt_debug_plan(hykkt_t h, int32_t* order, int32_t* first, int32_t* nrows, 
 // Diagnostics: one traced H^-1 pass (b = r_hat_x of the last KKT solve);
 // out[t] / out[2 nsup + t] = end / start time (ns) of task t (t < nsup:
 // forward task of order[t]; else backward task of order[2 nsup - 1 - t]).
+// Diagnostics: one k_trsv pass on r_hat (w solve); copies the permuted
+// forward (y) and backward (x) results to the host.
+int hykkt_debug_trsv_vectors(hykkt_t h, double* y, double* x) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_factor || !c.have_kkt) throw StateError("needs a factored KKT system");
+    run_trsv(c, c.rhat.p, nullptr, c.js.p, nullptr);
+    read_status(c);
+    CK(cudaMemcpy(y, c.y.p, c.sp.n * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(x, c.xsol.p, c.sp.n * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
 // Diagnostics: one k_trsv pass (w solve) with per-CTA phase stamps
 // (8 per CTA: start, after rearm barrier, after the forward bottom levels,
 // task loop exit, after the backward bottom barrier, after backward bottom /

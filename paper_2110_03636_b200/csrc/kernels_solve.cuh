@@ -136,6 +136,13 @@ struct TrsvArgs {
   const int* chain_ptr;
   const int* chain_sn;
   const int* nar_bwd;  // backward order of the narrow stream (chains at their top member)
+  // register hand-off tables of the chains (per row slot): forward, member
+  // i > 0, row q: the lane of member i-1 holding the row's update value
+  // (-1: none); backward, member i < top, rows below: lane | kind << 8 of
+  // member i+1's registers holding that row's x (kind 0: its own columns,
+  // 1: its rows below)
+  const int* chain_fsrc;
+  const int* chain_bsrc;
 };
 
 #ifndef HYKKT_INLINE_MID
@@ -919,6 +926,159 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
   }
 }
 
+// A chain of single-child narrow supernodes (w <= 4, rows <= 32, at most
+// 32 members), forward, one warp: member i+1's static data (panel rows,
+// right-hand side, reciprocal diagonal, hand-off lanes) is loaded while
+// member i is solved, and member i's update values reach member i+1 by
+// shuffles (chain_fsrc), so a chain link costs no memory round trip.  Only
+// the lowest member gathers (and polls) its children's update vectors, and
+// only the top member stores its update vector.  Same arithmetic as
+// fwd_task's narrow branch.
+struct ChainStatic {
+  double l[4], b, rd;
+  int src;
+};
+
+__device__ __forceinline__ void chain_fwd_static(const TrsvArgs& a, int f, int w, int nr, int rp, int off,
+                                                 int lane, bool first, ChainStatic& c) {
+  const double* P = a.panel + off;
+  const bool own = lane < w, row = lane < nr;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c.l[k] = (row && k < w) ? __ldg(P + k * nr + lane) : 0.0;
+  c.b = own ? rhs_at(a, f + lane) : 0.0;
+  c.rd = own ? 1.0 / __ldg(P + lane * nr + lane) : 1.0;
+  c.src = (!first && row) ? __ldg(a.chain_fsrc + rp + lane) : -1;
+}
+
+__device__ __noinline__ void chain_fwd(const TrsvArgs& a, const int* cs, int cn, int lane) {
+  const SnPlan& s = a.s;
+  // lane k holds member k's supernode and metadata
+  const int msn = cs[min(lane, cn - 1)];
+  const int mf = s.first[msn], mw = s.first[msn + 1] - mf, mnr = s.nrows[msn];
+  const int mrp = s.rows_ptr[msn], moff = s.off[msn], mu = s.u_off[msn];
+  ChainStatic cur, nxt;
+  chain_fwd_static(a, __shfl_sync(0xffffffffu, mf, 0), __shfl_sync(0xffffffffu, mw, 0),
+                   __shfl_sync(0xffffffffu, mnr, 0), __shfl_sync(0xffffffffu, mrp, 0),
+                   __shfl_sync(0xffffffffu, moff, 0), lane, true, cur);
+  double prev = 0.0;
+  for (int i = 0; i < cn; ++i) {
+    const int f = __shfl_sync(0xffffffffu, mf, i), w = __shfl_sync(0xffffffffu, mw, i);
+    const int nr = __shfl_sync(0xffffffffu, mnr, i), rp = __shfl_sync(0xffffffffu, mrp, i);
+    if (i + 1 < cn)
+      chain_fwd_static(a, __shfl_sync(0xffffffffu, mf, i + 1), __shfl_sync(0xffffffffu, mw, i + 1),
+                       __shfl_sync(0xffffffffu, mnr, i + 1), __shfl_sync(0xffffffffu, mrp, i + 1),
+                       __shfl_sync(0xffffffffu, moff, i + 1), lane, false, nxt);
+    const bool own = lane < w, row = lane < nr;
+    double acc = 0.0;
+    if (i == 0) {
+      const int sn = cs[0];
+      if (a.pre_wait & 1) wait_children(a, sn, lane);
+      if (row) acc = gather_u(a, __ldg(s.gat_ptr + rp + lane), __ldg(s.gat_ptr + rp + lane + 1));
+    } else {
+      const double v = __shfl_sync(0xffffffffu, prev, cur.src >= 0 ? cur.src : 0);
+      acc = cur.src >= 0 ? 0.0 + v : 0.0;
+    }
+    acc = own ? cur.b - acc : acc;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < w) {
+        const double yk = __shfl_sync(0xffffffffu, acc * cur.rd, k);
+        if (lane == k) acc = yk;
+        if (lane > k && lane < w) acc = fma(-cur.l[k], yk, acc);
+        if (lane >= w && row) acc = fma(cur.l[k], yk, acc);
+      }
+    }
+    const int uo = __shfl_sync(0xffffffffu, mu, i);  // (every lane: full-mask shuffle)
+    if (own) stcg(a.y + f + lane, acc);
+    if (i == cn - 1 && lane >= w && row) stcg(a.u + uo + lane - w, acc);
+    prev = acc;
+    cur = nxt;
+  }
+}
+
+// Backward counterpart: top member first (x of its rows from memory,
+// polled), then down the chain with each member's x of the rows below
+// taken from the previous member's registers (chain_bsrc): the member's
+// own columns (kind 0) or the rows it had loaded (kind 1).
+struct ChainStaticB {
+  double lv[4], ld[4], rd, y;
+  int src;
+};
+
+__device__ __forceinline__ void chain_bwd_static(const TrsvArgs& a, int f, int w, int nr, int rp, int off,
+                                                 int lane, bool top, ChainStaticB& c) {
+  const double* P = a.panel + off;
+  const int below = nr - w;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    c.lv[k] = (lane < below && k < w) ? __ldg(P + k * nr + w + lane) : 0.0;
+    c.ld[k] = (lane < w && k < w) ? __ldg(P + lane * nr + k) : 0.0;
+  }
+  c.rd = lane < w ? 1.0 / __ldg(P + lane * nr + lane) : 1.0;
+  // y is complete once the top member's parent values are (the backward of
+  // the chain starts after every forward task); the top member loads it
+  // after that wait, the others are prefetched after it
+  c.y = (!top && lane < w) ? ldcg(a.y + f + lane) : 0.0;
+  c.src = lane < below ? (top ? __ldg(a.s.rows + rp + w + lane) : __ldg(a.chain_bsrc + rp + w + lane)) : -1;
+}
+
+__device__ __noinline__ void chain_bwd(const TrsvArgs& a, const int* cs, int cn, int lane) {
+  const SnPlan& s = a.s;
+  const int msn = cs[min(lane, cn - 1)];
+  const int mf = s.first[msn], mw = s.first[msn + 1] - mf, mnr = s.nrows[msn];
+  const int mrp = s.rows_ptr[msn], moff = s.off[msn];
+  const int t0 = cn - 1;
+  ChainStaticB cur, nxt;
+  chain_bwd_static(a, __shfl_sync(0xffffffffu, mf, t0), __shfl_sync(0xffffffffu, mw, t0),
+                   __shfl_sync(0xffffffffu, mnr, t0), __shfl_sync(0xffffffffu, mrp, t0),
+                   __shfl_sync(0xffffffffu, moff, t0), lane, true, cur);
+  double pacc = 0.0, pxr = 0.0;
+  for (int i = cn - 1; i >= 0; --i) {
+    const int f = __shfl_sync(0xffffffffu, mf, i), w = __shfl_sync(0xffffffffu, mw, i);
+    const int nr = __shfl_sync(0xffffffffu, mnr, i), below = nr - w;
+    double xr = 0.0;
+    if (i == cn - 1) {
+      if (a.pre_wait & 4) wait_parent(a, cs[i], lane);
+      xr = lane < below ? load_ready(a.x + cur.src, a.abort) : 0.0;
+      if (lane < w) cur.y = load_ready(a.y + f + lane, a.abort);
+    }
+    // the next member's static data (its y is complete from here on)
+    if (i > 0)
+      chain_bwd_static(a, __shfl_sync(0xffffffffu, mf, i - 1), __shfl_sync(0xffffffffu, mw, i - 1),
+                       __shfl_sync(0xffffffffu, mnr, i - 1), __shfl_sync(0xffffffffu, mrp, i - 1),
+                       __shfl_sync(0xffffffffu, moff, i - 1), lane, false, nxt);
+    if (i != cn - 1) {
+      const int sl = cur.src & 0xff;
+      const double vo = __shfl_sync(0xffffffffu, pacc, cur.src >= 0 ? sl : 0);
+      const double vb = __shfl_sync(0xffffffffu, pxr, cur.src >= 0 ? sl : 0);
+      xr = cur.src < 0 ? 0.0 : ((cur.src >> 8) ? vb : vo);
+    }
+    double acc = lane < w ? cur.y : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < w) {
+        const double t = warp_sum(cur.lv[k] * xr);
+        if (lane == k) acc -= t;
+      }
+    }
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      if (k < w) {
+        const double xk = __shfl_sync(0xffffffffu, acc * cur.rd, k);
+        if (lane == k) acc = xk;
+        if (lane < k) acc = fma(-cur.ld[k], xk, acc);
+      }
+    }
+    if (lane < w) {
+      stcg(a.x + f + lane, acc);
+      if (a.x_out) a.x_out[s.perm[f + lane]] = acc;
+    }
+    pacc = acc;
+    pxr = xr;
+    cur = nxt;
+  }
+}
+
 // The narrow-stream tasks as real calls (trsv_pass<true>): a smaller task
 // loop, separately allocated registers and the medium (w <= 16) branches;
 // measured faster on the smaller trees (C1-C3) together with pre-wait on
@@ -989,6 +1149,12 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
       // supernodes, solved in order by this warp (forward bottom-up,
       // backward top-down) with no hand-off to another warp in between
       const int c0 = e >= 0 ? 0 : a.chain_ptr[-e - 1], cn = e >= 0 ? 1 : a.chain_ptr[-e] - c0;
+      if (CALL && e < 0 && a.chain_fsrc) {  // register hand-off along the chain
+        if (fwd) chain_fwd(a, a.chain_sn + c0, cn, lane);
+        else chain_bwd(a, a.chain_sn + c0, cn, lane);
+        __syncwarp();
+        continue;
+      }
       for (int ci = 0; ci < cn; ++ci) {
         const int sn = e >= 0 ? e : a.chain_sn[c0 + (fwd ? ci : cn - 1 - ci)];
         const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
