@@ -21,7 +21,7 @@ namespace hykkt::dev {
 
 struct BDims {
   int B;    // real systems
-  int Bp;   // padded stride (multiple of 32)
+  int Bp;   // padded stride (a power of two >= 32: index splits are shifts / masks)
   int T;    // tiles = Bp / 32
 };
 
@@ -86,8 +86,8 @@ struct BVals {  // interleaved inputs
 // ---- assembly ---------------------------------------------------------------
 __global__ void kb_reduce(AsmPlan p, BDims bd, BVals v, double* __restrict__ ht, double* __restrict__ r_x) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int b = static_cast<int>(g % bd.Bp);
-  const long long t = g / bd.Bp;
+  const int b = static_cast<int>(g & (bd.Bp - 1));
+  const long long t = (g >> (__ffs(bd.Bp) - 1));
   const int Bp = bd.Bp;
   if (t < p.n_ht) {
     const int col = p.ht_col[t];
@@ -148,9 +148,9 @@ __global__ void kb_ruiz(BRuizArgs a) {
     grid_sync(a.bar, a.abort);
     const long long nh = (long long)a.p.n_ht * Bp;
     for (long long g = gt; g < nh; g += gs) {
-      const int b = static_cast<int>(g % Bp);
+      const int b = static_cast<int>(g & (Bp - 1));
       if (it > 1 && !ldcg_int(prev + b)) continue;
-      const long long t = g / Bp;
+      const long long t = (g >> (__ffs(Bp) - 1));
       const int i = a.p.ht_row[t], j = a.p.ht_col[t];
       const double v = __dmul_rn(__dmul_rn(fabs(a.ht[g]), ldcg(a.d + bidx(i, Bp, b))), ldcg(a.d + bidx(j, Bp, b)));
       atomic_max_nonneg(a.norms + bidx(i, Bp, b), v);
@@ -158,9 +158,9 @@ __global__ void kb_ruiz(BRuizArgs a) {
     }
     const long long nj = (long long)a.p.nnz_j * Bp;
     for (long long g = gt; g < nj; g += gs) {
-      const int b = static_cast<int>(g % Bp);
+      const int b = static_cast<int>(g & (Bp - 1));
       if (it > 1 && !ldcg_int(prev + b)) continue;
-      const long long q = g / Bp;
+      const long long q = (g >> (__ffs(Bp) - 1));
       const int k = a.p.j_ri[q], j = a.p.j_col[q];
       const double v = __dmul_rn(__dmul_rn(fabs(a.jval[g]), ldcg(a.d + bidx(a.p.nx + k, Bp, b))),
                                  ldcg(a.d + bidx(j, Bp, b)));
@@ -170,7 +170,7 @@ __global__ void kb_ruiz(BRuizArgs a) {
     grid_sync(a.bar, a.abort);
     int* cur = a.unconverged + it * Bp;
     for (long long g = gt; g < nrow; g += gs) {
-      const int b = static_cast<int>(g % Bp);
+      const int b = static_cast<int>(g & (Bp - 1));
       if (it > 1 && !ldcg_int(prev + b)) continue;
       const double v = ldcg(a.norms + g);
       if (v > 0.0 && fabs(v - 1.0) > a.tol) atomicOr(cur + b, 1);
@@ -182,7 +182,7 @@ __global__ void kb_ruiz(BRuizArgs a) {
       if (ldcg_int(cur + b)) atomicAdd(a.active_count + it, 1);
     }
     for (long long g = gt; g < nrow; g += gs) {
-      const int b = static_cast<int>(g % Bp);
+      const int b = static_cast<int>(g & (Bp - 1));
       if (!ldcg_int(cur + b)) continue;
       const double v = ldcg(a.norms + g);
       if (v > 0.0) a.d[g] = __ddiv_rn(ldcg(a.d + g), __dsqrt_rn(v));
@@ -219,9 +219,9 @@ __global__ void kb_ruiz_rows(BRuizRowsArgs ar) {
     const int* prev = a.unconverged + (it - 1) * Bp;
     int* cur = a.unconverged + it * Bp;
     for (long long g = gt; g < nrow; g += gs) {
-      const int b = static_cast<int>(g % Bp);
+      const int b = static_cast<int>(g & (Bp - 1));
       if (it > 1 && !ldcg_int(prev + b)) continue;
-      const int i = static_cast<int>(g / Bp);
+      const int i = static_cast<int>((g >> (__ffs(Bp) - 1)));
       double nm = 0.0;
       for (int e = __ldg(ar.rp + i), e1 = __ldg(ar.rp + i + 1); e < e1; ++e) {
         const int4 q = __ldg(ar.ent + e);
@@ -238,7 +238,7 @@ __global__ void kb_ruiz_rows(BRuizRowsArgs ar) {
       if (ldcg_int(cur + b)) atomicAdd(a.active_count + it, 1);
     }
     for (long long g = gt; g < nrow; g += gs) {
-      const int b = static_cast<int>(g % Bp);
+      const int b = static_cast<int>(g & (Bp - 1));
       if (!ldcg_int(cur + b)) continue;
       const double v = ldcg(a.norms + g);
       if (v > 0.0) a.d[g] = __ddiv_rn(ldcg(a.d + g), __dsqrt_rn(v));
@@ -253,8 +253,8 @@ __global__ void kb_scale(AsmPlan p, BDims bd, const double* __restrict__ d, cons
                          const double* __restrict__ r_y, double* __restrict__ hts, double* __restrict__ js,
                          double* __restrict__ js_csr, double* __restrict__ rxs, double* __restrict__ rys) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
-  const long long t = g / Bp;
+  const int Bp = bd.Bp, b = static_cast<int>(g & (Bp - 1));
+  const long long t = (g >> (__ffs(Bp) - 1));
   if (t < p.n_ht) hts[g] = __dmul_rn(ht[g], __dmul_rn(d[bidx(p.ht_row[t], Bp, b)], d[bidx(p.ht_col[t], Bp, b)]));
   if (t < p.nnz_j) {
     js[g] = __dmul_rn(jval[g], __dmul_rn(d[bidx(p.nx + p.j_ri[t], Bp, b)], d[bidx(p.j_col[t], Bp, b)]));
@@ -270,8 +270,8 @@ __global__ void kb_hgamma(AsmPlan p, BDims bd, double gamma, const double* __res
                           const double* __restrict__ rys, double* __restrict__ hg, double* __restrict__ rhat,
                           double* __restrict__ maxdiag) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
-  const long long t = g / Bp;
+  const int Bp = bd.Bp, b = static_cast<int>(g & (Bp - 1));
+  const long long t = (g >> (__ffs(Bp) - 1));
   if (t < p.n_hg) {
     const int src = p.hg_src[t];
     double v = (src >= 0) ? __dadd_rn(0.0, hts[bidx(src, Bp, b)]) : 0.0;
@@ -298,8 +298,8 @@ __global__ void kb_scatter(int nsrc, BDims bd, SnPlan sp, const int* __restrict_
                            const double* __restrict__ delta1, const int* __restrict__ active,
                            double* __restrict__ panel) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
-  const long long t = g / Bp;
+  const int Bp = bd.Bp, b = static_cast<int>(g & (Bp - 1));
+  const long long t = (g >> (__ffs(Bp) - 1));
   if (t >= nsrc || !active[b]) return;
   double v = src[g];
   const double d1 = delta1[b];
@@ -313,9 +313,9 @@ __global__ void kb_zero_panels(long long nslots, BDims bd, SnPlan sp, const int*
                                double* __restrict__ panel) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (g >= nslots * bd.Bp) return;
-  const int b = static_cast<int>(g % bd.Bp);
+  const int b = static_cast<int>(g & (bd.Bp - 1));
   if (!active[b]) return;
-  const int p = static_cast<int>(g / bd.Bp), sn = slot_sn[p];
+  const int p = static_cast<int>((g >> (__ffs(bd.Bp) - 1))), sn = slot_sn[p];
   panel[pan_addr(sp, mode, sn, p - sp.off[sn], bd.Bp, b)] = 0.0;
 }
 
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(256) kb_factor(BFactorArgs a) {
     const int i0 = __ldg(a.job_ptr + j), i1 = __ldg(a.job_ptr + j + 1);
     if (a.job_kind[j]) {
       const int it = __ldg(a.job_items + i0);
-      wfactor_task(a, it / Bp, it % Bp, bsmem);
+      wfactor_task(a, (it >> (__ffs(Bp) - 1)), (it & (Bp - 1)), bsmem);
     } else if (i0 + wid < i1) {
       const int t = __ldg(a.job_items + i0 + wid);
       bfactor_task(a, a.s.order[t / T], t % T, lane);
@@ -1024,8 +1024,8 @@ __device__ __forceinline__ void btrsv_pass(const BTrsvArgs& a) {
     if (kind) {
       const int it = __ldg(a.job_items + i0);
       if (a.trace && threadIdx.x == 0) a.trace[a.njobs + j] = global_ns();
-      if (kind == 1) wfwd_task(a, it / a.bd.Bp, it % a.bd.Bp, bsmem);
-      else wbwd_task(a, it / a.bd.Bp, it % a.bd.Bp, bsmem);
+      if (kind == 1) wfwd_task(a, (it >> (__ffs(a.bd.Bp) - 1)), (it & (a.bd.Bp - 1)), bsmem);
+      else wbwd_task(a, (it >> (__ffs(a.bd.Bp) - 1)), (it & (a.bd.Bp - 1)), bsmem);
       if (a.trace && threadIdx.x == 0) a.trace[j] = global_ns();
     } else if (i0 + wid < i1) {
       const long long t = __ldg(a.job_items + i0 + wid);
@@ -1053,8 +1053,8 @@ __global__ void __launch_bounds__(256) kb_trsv(BTrsvArgs a) {
 __global__ void kb_schur_rhs(int mc, BDims bd, const int* rp, const int* ci_perm, const double* jcsr,
                              const double* y, const double* r_y, double* rhs) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
-  const long long k = g / Bp;
+  const int Bp = bd.Bp, b = static_cast<int>(g & (Bp - 1));
+  const long long k = (g >> (__ffs(Bp) - 1));
   if (k >= mc) return;
   double acc = 0.0;
   for (int e = rp[k]; e < rp[k + 1]; ++e) {
@@ -1151,7 +1151,7 @@ __global__ void __launch_bounds__(256) kb_cg(BCgArgs a) {
     double pq = 0.0, pp = 0.0;
     for (long long g = gt; g < mcB; g += gs) {
       if (!run) continue;
-      const long long k = g / Bp;
+      const long long k = (g >> (__ffs(Bp) - 1));
       double qk = 0.0;
       for (int e = a.jcsr_rp[k]; e < a.jcsr_rp[k + 1]; ++e) {
         const double t = ldcg(tr.x + bidx(a.jcsr_ci_perm[e], Bp, b));
@@ -1214,8 +1214,8 @@ __global__ void kb_recover(AsmPlan p, BDims bd, const int* __restrict__ jd_rp, c
                            double* __restrict__ dx, double* __restrict__ dy, double* __restrict__ ds,
                            double* __restrict__ dyd) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int Bp = bd.Bp, b = static_cast<int>(g % Bp);
-  const long long t = g / Bp;
+  const int Bp = bd.Bp, b = static_cast<int>(g & (Bp - 1));
+  const long long t = (g >> (__ffs(Bp) - 1));
   if (t < p.nx) dx[g] = __dmul_rn(d[g], dx_s[g]);
   if (t < p.mc) dy[g] = __dmul_rn(d[bidx(p.nx + t, Bp, b)], dy_s[g]);
   if (t < p.md) {
