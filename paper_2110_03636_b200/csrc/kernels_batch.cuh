@@ -753,7 +753,7 @@ __device__ __forceinline__ void bfwd_core(const BTrsvArgs& a, int sn, int b, dou
         for (int j = 0; j < kC; ++j) {
           if (j < k) acc = fma(-__ldg(P + (long long)((cb + j) * nr + cb + k) * Bp), yv[j], acc);
         }
-        yv[k] = acc / __ldg(P + (long long)((cb + k) * nr + cb + k) * Bp);
+        yv[k] = acc * (1.0 / __ldg(P + (long long)((cb + k) * nr + cb + k) * Bp));
         stcg(a.y + bidx(f + cb + k, Bp, b), yv[k]);
       }
     }
@@ -851,7 +851,7 @@ __device__ void bbwd_task(const BTrsvArgs& a, int sn, int tile, int lane) {
         for (int j = 0; j < kC; ++j) {
           if (j > k && j < cw) acc = fma(-__ldg(P + (long long)((cb + k) * nr + cb + j) * Bp), xc[j], acc);
         }
-        xc[k] = acc / __ldg(P + (long long)((cb + k) * nr + cb + k) * Bp);
+        xc[k] = acc * (1.0 / __ldg(P + (long long)((cb + k) * nr + cb + k) * Bp));
         stcg(a.x + bidx(f + cb + k, Bp, b), xc[k]);
         if (a.x_out) a.x_out[bidx(s.perm[f + cb + k], Bp, b)] = xc[k];
       }
@@ -913,10 +913,11 @@ __device__ void wfwd_task(const BTrsvArgs& a, int sn, int b, double* sm) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) d[k] = (k < cw && lane < cw) ? P[(cb + k) * nr + cb + lane] : 0.0;
       double acc = lane < cw ? V[cb + lane] : 0.0;
+      const double rdl = lane < cw ? 1.0 / P[(cb + lane) * nr + cb + lane] : 1.0;
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         if (k < cw) {
-          const double yk = __shfl_sync(0xffffffffu, acc, k) / __shfl_sync(0xffffffffu, d[k], k);
+          const double yk = __shfl_sync(0xffffffffu, acc * rdl, k);
           if (lane == k) acc = yk;
           if (lane > k && lane < cw) acc = fma(-d[k], yk, acc);
         }
@@ -978,10 +979,11 @@ __device__ void wbwd_task(const BTrsvArgs& a, int sn, int b, double* sm) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) d[j] = (j < cw && lane < cw) ? P[(cb + lane) * nr + cb + j] : 0.0;
       double acc = lane < cw ? load_ready(a.y + bidx(f + cb + lane, Bp, b), a.abort) - S[cb + lane] : 0.0;
+      const double rdl = lane < cw ? 1.0 / P[(cb + lane) * nr + cb + lane] : 1.0;
 #pragma unroll
       for (int j = 31; j >= 0; --j) {
         if (j < cw) {
-          const double xj = __shfl_sync(0xffffffffu, acc, j) / __shfl_sync(0xffffffffu, d[j], j);
+          const double xj = __shfl_sync(0xffffffffu, acc * rdl, j);
           if (lane == j) acc = xj;
           if (lane < j) acc = fma(-d[j], xj, acc);
         }
