@@ -768,7 +768,11 @@ __global__ void __launch_bounds__(256) k_qform(int nrows_total, const int2* __re
   double v[NC];
 #pragma unroll
   for (int i = 0; i < NC; ++i) v[i] = 0.0;
-  for (int k = w - 1; k >= 0; --k) {
+  // own rows: M = L_ss^-1 is lower triangular, Q[qr, k] = 0 for k > qr
+  for (int k = qr < w ? qr : w - 1; k >= 0; --k) {
+    // the reciprocal diagonal does not depend on the chain (no FP64 division on it)
+    const double rd = 1.0 / __ldg(P + static_cast<long long>(k) * nr + k);
+    const double e = qr < w ? (qr == k ? 1.0 : 0.0) : __ldg(P + static_cast<long long>(k) * nr + qr);
     double t = 0.0;
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -776,8 +780,7 @@ __global__ void __launch_bounds__(256) k_qform(int nrows_total, const int2* __re
       if (j > k && j < w) t = fma(v[i], __ldg(P + static_cast<long long>(k) * nr + j), t);
     }
     t = warp_sum(t);
-    const double e = qr < w ? (qr == k ? 1.0 : 0.0) : __ldg(P + static_cast<long long>(k) * nr + qr);
-    const double qk = (e - t) / __ldg(P + static_cast<long long>(k) * nr + k);
+    const double qk = (e - t) * rd;
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
       if (lane + 32 * i == k) v[i] = qk;
