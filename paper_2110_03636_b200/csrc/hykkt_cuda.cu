@@ -119,7 +119,7 @@ struct hykkt_context {
   hykkt::DBuf<double> mf_ubuf;
   int mf_ntasks = 0, mf_on = 1;
   // single-system triangular-solve task streams (kernels_solve.cuh trsv_pass)
-  hykkt::DBuf<int> tr_wid, tr_nar, tr_nar_bwd, tr_pos, tr_chain_ptr, tr_chain_sn, tr_chain_fsrc, tr_chain_bsrc;
+  hykkt::DBuf<int> tr_bt_rows, tr_wid, tr_wid_bwd, tr_nar, tr_nar_bwd, tr_pos, tr_chain_ptr, tr_chain_sn, tr_chain_fsrc, tr_chain_bsrc;
   int tr_chain_regs = 0;
   int tr_nwid = 0, tr_nnar = 0, tr_nbot = 0;
   int tr_call = 0;  // narrow tasks as real calls (trsv_pass<true>), chosen per analysis
@@ -147,6 +147,9 @@ struct hykkt_context {
   hykkt::DBuf<double> cl_vals;
   int cl_nvals = 0;
   hykkt::DBuf<double> cl_bt;
+  hykkt::DBuf<double> cg_bt;  // k_cg: precomputed forward right-hand side (TrsvArgs::bt_fill)
+  int tr_nbt_rows = 0;
+  int cg_bt_on = 0;
   hykkt::DBuf<unsigned long long> cl_stamps;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
@@ -392,18 +395,39 @@ void init_ctx(Ctx& c, int device) {
 
 // Level-ordered CTA task list: supernodes with big(sn) are single-supernode
 // (whole CTA) tasks, the others are grouped per level, up to one per warp.
+// Depth of every supernode below the root of its tree (s.order lists
+// children before parents).
+std::vector<int> sn_depth(const SupernodalPlan& s) {
+  std::vector<int> depth(s.nsup, 0);
+  for (idx q = s.nsup - 1; q >= 0; --q) {
+    const int sn = s.order[q], p = s.sn_parent[sn];
+    depth[sn] = p < 0 ? 0 : depth[p] + 1;
+  }
+  return depth;
+}
+
 template <class Pred>
 void level_tasks(const SupernodalPlan& s, Pred big, std::vector<int>& tp, std::vector<int>& tsn,
-                 std::vector<unsigned char>& tbig) {
+                 std::vector<unsigned char>& tbig, bool by_depth = false) {
   tp.assign(1, 0);
   tsn.clear();
   tbig.clear();
+  // by_depth: descending depth below the root instead of ascending level
+  // (both topological; supernodes sharing a key never depend on each other)
+  std::vector<int> seq(s.order.begin(), s.order.end()), key(s.nsup);
+  if (by_depth) {
+    const std::vector<int> depth = sn_depth(s);
+    std::stable_sort(seq.begin(), seq.end(), [&](int x, int y) { return depth[x] > depth[y]; });
+    for (idx k = 0; k < s.nsup; ++k) key[k] = -depth[k];
+  } else {
+    for (idx k = 0; k < s.nsup; ++k) key[k] = s.sn_level[k];
+  }
   idx q = 0;
   while (q < s.nsup) {
-    const int lev = s.sn_level[s.order[q]];
+    const int lev = key[seq[q]];
     std::vector<int> narrow;
-    for (; q < s.nsup && s.sn_level[s.order[q]] == lev; ++q) {
-      const int sn = s.order[q];
+    for (; q < s.nsup && key[seq[q]] == lev; ++q) {
+      const int sn = seq[q];
       if (big(sn)) {
         tsn.push_back(sn);
         tp.push_back(static_cast<int>(tsn.size()));
@@ -676,7 +700,11 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     }
     std::vector<int> tp, tsn;
     std::vector<unsigned char> tbig;
-    level_tasks(s, [&](int sn) { return s.sn_nrows[sn] >= big_rows; }, tp, tsn, tbig);
+    // descending depth below the root (r02 A/B, bit-identical: factor C3
+    // 1.75 -> 1.54 ms, C4 10.56 -> 9.94 ms, C2 within 1 %)
+    bool by_depth = true;
+    if (const char* e = std::getenv("HYKKT_MF_ORDER")) by_depth = std::atoi(e) == 1;
+    level_tasks(s, [&](int sn) { return s.sn_nrows[sn] >= big_rows; }, tp, tsn, tbig, by_depth);
     c.mf_uoff.upload(uo, st);
     c.mf_task_ptr.upload(tp, st);
     c.mf_task_sn.upload(tsn.empty() ? std::vector<int>{0} : tsn, st);
@@ -733,11 +761,46 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     c.tr_nbot = nbot;
     c.tr_bot_ptr.upload(bptr, st);
     c.tr_bot_sn.upload(bsn.empty() ? std::vector<int>{0} : bsn, st);
-    std::vector<int> wid, nar;
+    // Task-stream orders.  Backward: parents before children by descending
+    // level (height above the leaves: the longest remaining path first).
+    // Forward: either ascending level, or (HYKKT_TRSV_FWD_ORDER=1) by
+    // descending depth below the root, so the supernodes with the longest
+    // path still ahead of them (the deep chains under the top separators)
+    // are claimed first.  Both are topological; the wide and narrow streams
+    // of one pass always share the pass's order (deadlock freedom).
+    std::vector<int> fwd_seq(s.order.begin() + static_cast<std::ptrdiff_t>(bsn.size()), s.order.end());
+    {
+      // depth order above 32768 supernodes (r02 A/B, bit-identical results:
+      // C3 497 -> 451, C4 1383 -> 1157 us per CG iteration; C1 / C2 within 1 %)
+      int fo = s.nsup > 32768 ? 1 : 0;
+      if (const char* e = std::getenv("HYKKT_TRSV_FWD_ORDER")) fo = std::atoi(e);
+      if (fo == 1) {
+        const std::vector<int> depth = sn_depth(s);
+        std::stable_sort(fwd_seq.begin(), fwd_seq.end(), [&](int x, int y) { return depth[x] > depth[y]; });
+      }
+    }
+    {
+      // rows above the bottom levels (TrsvArgs::bt_rows)
+      std::vector<int> rows;
+      for (int sn : fwd_seq)
+        for (int r = s.sn_first[sn]; r < s.sn_first[sn + 1]; ++r) rows.push_back(r);
+      c.tr_nbt_rows = static_cast<int>(rows.size());
+      c.tr_bt_rows.upload(rows.empty() ? std::vector<int>{0} : rows, st);
+      c.cg_bt.alloc(std::max<idx>(1, s.n));
+      // on by default (r02 A/B, bit-identical: C1 226 -> 200, C2 281 -> 255,
+      // C3 466 -> 434, C4 1160 -> 1035 us per CG iteration)
+      c.cg_bt_on = 1;
+      if (const char* e = std::getenv("HYKKT_CG_BT")) c.cg_bt_on = std::atoi(e) != 0;
+    }
+    auto is_wide = [&](int sn) {
+      const long long w = s.sn_first[sn + 1] - s.sn_first[sn];
+      return s.sn_nrows[sn] <= dev::kWideMaxRows && w * s.sn_nrows[sn] >= wide;
+    };
+    std::vector<int> wid, nar, wid_lev, nar_lev;  // forward order / level order
+    for (int sn : fwd_seq) (is_wide(sn) ? wid : nar).push_back(sn);
     for (idx q = static_cast<idx>(bsn.size()); q < s.nsup; ++q) {
       const int sn = s.order[q];
-      const long long w = s.sn_first[sn + 1] - s.sn_first[sn];
-      (s.sn_nrows[sn] <= dev::kWideMaxRows && w * s.sn_nrows[sn] >= wide ? wid : nar).push_back(sn);
+      (is_wide(sn) ? wid_lev : nar_lev).push_back(sn);
     }
     // Q-form: every wide supernode (w <= kQMaxW) gets Q = [L_ss^-1; L_below
     // L_ss^-1] after each factorization and runs as independent row /
@@ -762,7 +825,7 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
           for (int qr = 0; qr < nr; ++qr) items.insert(items.end(), {sn, qr});
           for (int r0 = 0; r0 < nr; r0 += 32) sf.insert(sf.end(), {sn, r0, std::min(r0 + 32, nr), 0});
         }
-        for (auto it = wid.rbegin(); it != wid.rend(); ++it) {
+        for (auto it = wid_lev.rbegin(); it != wid_lev.rend(); ++it) {
           const int sn = *it, w = s.sn_first[sn + 1] - s.sn_first[sn];
           for (int c0 = 0; c0 < w; c0 += kThreads / 32) sb.insert(sb.end(), {sn, c0, std::min(c0 + kThreads / 32, w), 0});
         }
@@ -832,7 +895,7 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
         }
       }
       // backward order: reverse topological, each chain at its top member
-      for (auto it = nar.rbegin(); it != nar.rend(); ++it) {
+      for (auto it = nar_lev.rbegin(); it != nar_lev.rend(); ++it) {
         const int sn = *it;
         if (top_of[sn] >= 0) nar_bwd.push_back(-top_of[sn] - 1);
         else if (!link_up[sn] && !linked_from_below[sn]) nar_bwd.push_back(sn);
@@ -881,6 +944,8 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     c.tr_chain_ptr.upload(chain_ptr, st);
     c.tr_chain_sn.upload(chain_sn.empty() ? std::vector<int>{0} : chain_sn, st);
     c.tr_wid.upload(wid.empty() ? std::vector<int>{0} : wid, st);
+    std::vector<int> wid_bwd(wid_lev.rbegin(), wid_lev.rend());
+    c.tr_wid_bwd.upload(wid_bwd.empty() ? std::vector<int>{0} : wid_bwd, st);
     c.tr_nar.upload(nar.empty() ? std::vector<int>{0} : nar, st);
     c.tr_nwid = static_cast<int>(wid.size());
     c.tr_nnar = static_cast<int>(nar.size());
@@ -1015,6 +1080,7 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.trace = nullptr;
   ta.pstamp = nullptr;
   ta.wid_sn = c.tr_wid.p;
+  ta.wid_bwd = c.tr_wid_bwd.p;
   ta.nwid = c.tr_nwid;
   ta.nar_sn = c.tr_nar.p;
   ta.nnar = c.tr_nnar;
@@ -1035,6 +1101,14 @@ dev::TrsvArgs trsv_args(Ctx& c) {
     ta.pre_wait = c.tr_call ? 15 : 10;
     if (const char* e = std::getenv("HYKKT_TRSV_PREWAIT")) ta.pre_wait = std::atoi(e);
   }
+  ta.nshard = 1;
+  if (const char* e = std::getenv("HYKKT_TRSV_SHARDS")) ta.nshard = std::max(1, std::min(32, std::atoi(e)));
+  ta.tstride = 2 + 32 * ta.nshard;
+  ta.ahead = 0;
+  ta.bt_fill = nullptr;
+  ta.bt_rows = c.tr_bt_rows.p;
+  ta.nbt_rows = c.tr_nbt_rows;
+  if (const char* e = std::getenv("HYKKT_TRSV_AHEAD")) ta.ahead = std::atoi(e) != 0;
   ta.pos = c.tr_pos.p;
   ta.nbot = c.tr_nbot;
   ta.bot_ptr = c.tr_bot_ptr.p;
@@ -1101,7 +1175,11 @@ void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, doub
   ta.rhs.b = b;
   ta.rhs.u = u;
   ta.rhs.jval = jval;
-  ta.ticket = fresh_tickets(c, 2);
+  if (c.cg_bt_on) {
+    ta.bt_fill = c.cg_bt.p;
+    ta.bt = c.cg_bt.p;
+  }
+  ta.ticket = fresh_tickets(c, ta.tstride);
   coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
               &ta);
 }
@@ -1111,6 +1189,10 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   a.tr = trsv_args(c);
   a.tr.rhs.u = c.cg_p.p;
   a.tr.rhs.jval = c.js.p;
+  if (c.cg_bt_on) {
+    a.tr.bt_fill = c.cg_bt.p;
+    a.tr.bt = c.cg_bt.p;
+  }
   a.mc = static_cast<int>(c.kp.mc);
   a.jcsr_rp = c.jcsr_rp.p;
   a.jcsr_ci_perm = c.jcsr_ci_perm.p;
@@ -1149,7 +1231,7 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
     return read_status(c).cg;
   }
   ensure_qform(c);
-  a.tickets = fresh_tickets(c, 2 * (cfg.cg_max_iter + 2));
+  a.tickets = fresh_tickets(c, static_cast<long long>(a.tr.tstride) * (cfg.cg_max_iter + 2));
   coop_launch(c, c.tr_call ? (const void*)dev::k_cg<2, true> : c.cg_fn, c.coop_cg_blocks, &a);
   return read_status(c).cg;
 }
@@ -1884,6 +1966,17 @@ void build_batch_jobs(Ctx& c, int T) {
   for (long long k = 0; k < ns; ++k) {
     for (idx p = sp.sn_off[k]; p < sp.sn_off[k + 1]; ++p) slot_sn[p] = static_cast<int>(k);
   }
+  // factor / forward-solve job order: descending depth below the root, or
+  // (HYKKT_BATCH_ORDER=0) level order; both topological
+  std::vector<long long> fpos(ns);
+  for (long long k = 0; k < ns; ++k) fpos[k] = k;
+  // (r02 A/B on the bench batch: factor 11.23 -> 10.79 ms per step)
+  const char* bo = std::getenv("HYKKT_BATCH_ORDER");
+  if (!bo || std::atoi(bo) == 1) {
+    const std::vector<int> depth = sn_depth(sp);
+    std::stable_sort(fpos.begin(), fpos.end(),
+                     [&](long long x, long long y) { return depth[sp.order[x]] > depth[sp.order[y]]; });
+  }
   auto build = [&](bool solve, std::vector<int>& ptr, std::vector<int>& items, std::vector<unsigned char>& kind) {
     ptr.assign(1, 0);
     items.clear();
@@ -1897,8 +1990,11 @@ void build_batch_jobs(Ctx& c, int T) {
       group.clear();
     };
     for (int pass = 0; pass < (solve ? 2 : 1); ++pass) {
-      for (long long pos = 0; pos < ns; ++pos) {
-        const int sn = pass == 0 ? sp.order[pos] : sp.order[ns - 1 - pos];
+      for (long long k = 0; k < ns; ++k) {
+        // items encode the forward position / the backward loop index
+        // (kb_trsv decodes backward items as order[ns - 1 - index])
+        const long long pos = pass == 0 ? fpos[k] : k;
+        const int sn = pass == 0 ? sp.order[pos] : sp.order[ns - 1 - k];
         if (mode[sn]) {
           flush();
           for (int b = 0; b < Bp; ++b) {
@@ -3180,7 +3276,7 @@ int hykkt_debug_trsv_phases(hykkt_t h, uint64_t* out, int64_t cap, int64_t* nblk
       dev::TrsvArgs ta = trsv_args(c);
     ta.rhs.b = c.rhat.p;
     ta.pstamp = st.p;
-    ta.ticket = fresh_tickets(c, 2);
+    ta.ticket = fresh_tickets(c, ta.tstride);
     coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
                 &ta);
     read_status(c);
@@ -3221,7 +3317,7 @@ int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
       dev::TrsvArgs ta = trsv_args(c);
     ta.rhs.b = c.rhat.p;
     ta.trace = tr.p;
-    ta.ticket = fresh_tickets(c, 2);
+    ta.ticket = fresh_tickets(c, ta.tstride);
     coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
                 &ta);
     read_status(c);

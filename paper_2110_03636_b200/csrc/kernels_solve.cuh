@@ -102,7 +102,8 @@ struct TrsvArgs {
   unsigned long long* pstamp; // diagnostics: per-CTA phase times of k_trsv (8 per CTA), or null
   // task streams (trsv_pass): wide supernodes for the first nwc CTAs,
   // narrow ones for the warps of the others; ticket[0] / ticket[1]
-  const int* wid_sn;
+  const int* wid_sn;   // forward order
+  const int* wid_bwd;  // backward order
   int nwid;
   const int* nar_sn;
   int nnar;
@@ -143,6 +144,23 @@ struct TrsvArgs {
   // 1: its rows below)
   const int* chain_fsrc;
   const int* chain_bsrc;
+  // narrow-stream ticket shards: narrow task t belongs to shard t % nshard,
+  // whose counter is ticket[1 + 32 * shard] (one 128-byte line each); a warp
+  // serves shard (narrow warp index) % nshard.  Each shard is a subsequence
+  // of the topological order, so the smallest unfinished task is always
+  // claimed or claimable by its shard's warps: still deadlock-free.  tstride
+  // = counters per pass (k_cg: pass it uses ticket + tstride * it)
+  int nshard;
+  int tstride;
+  int ahead;  // narrow stream: claim the next entries while solving the current one
+  // forward right-hand side precomputed in the pass (k_cg): when bt_fill is
+  // set, the pass first writes bt_fill[r] = b - J^T u for the rows of every
+  // supernode above the bottom levels (bt_rows), alongside bottom level 0,
+  // and the tasks then read it through bt (= bt_fill); the bottom levels
+  // form their own rows' right-hand sides (rhs_raw)
+  double* bt_fill;
+  const int* bt_rows;
+  int nbt_rows;
 };
 
 #ifndef HYKKT_INLINE_MID
@@ -811,7 +829,7 @@ __device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
   for (int q = 0; q <= NR; ++q) gp[q] = q <= nr ? __ldg(s.gat_ptr + rp + q) : 0;
   double rb[W];
 #pragma unroll
-  for (int q = 0; q < W; ++q) rb[q] = q < w ? rhs_at(a, f + q) : 0.0;
+  for (int q = 0; q < W; ++q) rb[q] = q < w ? rhs_raw(a, f + q) : 0.0;
   int i0[NR], i1[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) {
@@ -915,6 +933,12 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   for (int li = 0; li < a.nbot; ++li) {
     const int l = fwd ? li : a.nbot - 1 - li;
+    if (fwd && li == 0 && a.bt_fill) {
+      for (int k = gt; k < a.nbt_rows; k += gs) {
+        const int r = __ldg(a.bt_rows + k);
+        a.bt_fill[r] = rhs_raw(a, r);
+      }
+    }
     const bool wide = a.bot_wide[l];
     for (int i = a.bot_ptr[l] + gt; i < a.bot_ptr[l + 1]; i += gs) {
       if (wide) {
@@ -1107,7 +1131,16 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int ns = a.s.nsup;
   unsigned long long* ps = (a.pstamp && threadIdx.x == 0) ? a.pstamp + 8 * blockIdx.x : nullptr;
-  if (a.nbot > 0) trsv_bottom(a, true);
+  if (a.nbot > 0) {
+    trsv_bottom(a, true);  // fills bt_fill with level 0 (a grid barrier follows)
+  } else if (a.bt_fill) {
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    for (int k = gt; k < a.nbt_rows; k += gs) {
+      const int r = __ldg(a.bt_rows + k);
+      a.bt_fill[r] = rhs_raw(a, r);
+    }
+    grid_sync(a.bar, a.abort);
+  }
   if (ps) ps[2] = global_ns();
   if (static_cast<int>(blockIdx.x) < a.nwc && a.nqf > 0) {
     // Q-form slices: forward row slices, then backward column slices
@@ -1135,7 +1168,7 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
       __syncthreads();
       if (t >= 2 * nt) break;
       const bool fwd = t < nt;
-      const int sn = a.wid_sn[fwd ? t : 2 * nt - 1 - t];
+      const int sn = fwd ? a.wid_sn[t] : a.wid_bwd[t - nt];
       const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
       if (a.trace && tid == 0) a.trace[2 * ns + slot] = global_ns();
       if (fwd) fwd_cta(a, S, sn);
@@ -1145,18 +1178,21 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
     }
   } else {
     const int nt = a.nnar;
-    for (long long t = grab_task(a.ticket + 1, lane); t < 2 * nt; t = grab_task(a.ticket + 1, lane)) {
+    const int nsh = a.nshard;
+    const int shard = (static_cast<int>(blockIdx.x - a.nwc) * static_cast<int>(blockDim.x >> 5) +
+                       static_cast<int>(threadIdx.x >> 5)) % nsh;
+    unsigned* const tk = a.ticket + 1 + 32 * shard;
+    // one narrow-stream entry: e >= 0 one supernode; e < 0 chain -e - 1 of
+    // single-child narrow supernodes, solved in order by this warp (forward
+    // bottom-up, backward top-down) with no hand-off to another warp
+    auto run_entry = [&](long long t, int e) {
       const bool fwd = t < nt;
-      const int e = fwd ? a.nar_sn[t] : a.nar_bwd[t - nt];
-      // e >= 0: one supernode; e < 0: chain -e - 1 of single-child narrow
-      // supernodes, solved in order by this warp (forward bottom-up,
-      // backward top-down) with no hand-off to another warp in between
       const int c0 = e >= 0 ? 0 : a.chain_ptr[-e - 1], cn = e >= 0 ? 1 : a.chain_ptr[-e] - c0;
       if (CALL && e < 0 && a.chain_fsrc) {  // register hand-off along the chain
         if (fwd) chain_fwd(a, a.chain_sn + c0, cn, lane);
         else chain_bwd(a, a.chain_sn + c0, cn, lane);
         __syncwarp();
-        continue;
+        return;
       }
       for (int ci = 0; ci < cn; ++ci) {
         const int sn = e >= 0 ? e : a.chain_sn[c0 + (fwd ? ci : cn - 1 - ci)];
@@ -1172,6 +1208,37 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
         if (a.trace && lane == 0) a.trace[slot] = global_ns();
         __syncwarp();
       }
+    };
+    const long long tend = 2ll * nt;
+    auto entry_of = [&](long long t) { return t < nt ? a.nar_sn[t] : a.nar_bwd[t - nt]; };
+    if (a.ahead) {
+      // Claims run ahead of the work: the warp holds its current entry, the
+      // next one (ticket resolved, entry index loaded while the current one
+      // is solved) and a claim in flight for the one after, so the ticket
+      // atomic and the entry lookup leave the per-task latency chain.  The
+      // tickets a warp holds increase, so the smallest unfinished entry is
+      // always its holder's current one: still deadlock-free.
+      unsigned r0 = 0, r1 = 0;
+      if (lane == 0) {
+        r0 = atomicAdd(tk, 1u);
+        r1 = atomicAdd(tk, 1u);
+      }
+      long long t = static_cast<long long>(__shfl_sync(0xffffffffu, r0, 0)) * nsh + shard;
+      long long t1 = static_cast<long long>(__shfl_sync(0xffffffffu, r1, 0)) * nsh + shard;
+      int e = t < tend ? entry_of(t) : 0;
+      while (t < tend) {
+        const int e1 = t1 < tend ? entry_of(t1) : 0;
+        unsigned r2 = 0;
+        if (lane == 0 && t1 < tend) r2 = atomicAdd(tk, 1u);
+        run_entry(t, e);
+        const long long t2 = static_cast<long long>(__shfl_sync(0xffffffffu, r2, 0)) * nsh + shard;
+        t = t1;
+        e = e1;
+        t1 = t < tend ? t2 : tend;
+      }
+    } else {
+      for (long long t = grab_task(tk, lane) * nsh + shard; t < tend; t = grab_task(tk, lane) * nsh + shard)
+        run_entry(t, entry_of(t));
     }
   }
   if (ps) ps[3] = global_ns();
@@ -1294,7 +1361,7 @@ __global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
   double r_norm = rhs_norm;
   TrsvArgs tr = a.tr;
   for (long long it = 1; it <= a.max_iter; ++it) {
-    tr.ticket = a.tickets + 2 * it;
+    tr.ticket = a.tickets + static_cast<long long>(tr.tstride) * it;
     trsv_pass<CALL>(tr, S);
     grid_sync(bar, abort);
     double pq = 0.0, pp = 0.0;

@@ -48,3 +48,8 @@ for k in chain[:25]:
     p = parent[k]
     pe = bend[p] if p >= 0 else fend[k]
     print("  %6d %4d %4d %8.1f %7.1f detect %7.2f compute %7.2f" % (k, width[k], nrows[k], bend[k], bend[k] - pe, bready[k] - pe, bend[k] - bready[k]))
+# raw per-supernode times for offline analysis (tools/trace_levels.py)
+import os
+if os.environ.get("TRACE_NPZ"):
+    np.savez_compressed(os.environ["TRACE_NPZ"], fstart=fstart, fready=fready, fend=fend, bstart=bstart,
+                        bready=bready, bend=bend, width=width, nrows=nrows, parent=parent, order=order)
