@@ -60,6 +60,13 @@ __device__ __forceinline__ void warp_publish(int* flag, int value, int lane) {
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ int ldcg_int(const int* p) { return __ldcg(p); }
 __device__ __forceinline__ void stcg(double* p, double v) { __stcg(p, v); }
+// Warp-cooperative L1 prefetch of [p, p + bytes): one 128-byte line per lane
+// per round, issued before a wait so later __ldg loads of static data hit L1.
+__device__ __forceinline__ void prefetch_l1(const void* p, long long bytes, int lane) {
+  const char* b = reinterpret_cast<const char*>(reinterpret_cast<unsigned long long>(p) & ~127ull);
+  const char* e = reinterpret_cast<const char*>(p) + bytes;
+  for (const char* q = b + 128 * lane; q < e; q += 128 * 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+}
 
 // Waits until *flag == want. Returns false (and raises *abort) on timeout
 // or when another waiter already aborted.  The shared abort word and the

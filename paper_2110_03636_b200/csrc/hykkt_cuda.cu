@@ -1095,20 +1095,25 @@ dev::TrsvArgs trsv_args(Ctx& c) {
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
     nwc = std::min({nwc, c.tr_nwid, std::max(1, c.coop_cg_blocks / 2)});
     ta.nwc = c.tr_nwid > 0 ? nwc : 0;
+    // dedicated wide CTAs (the rest of the nwc help with the narrow forward
+    // stream first); at least one
+    int nwd = ta.nwc;
+    if (const char* e = std::getenv("HYKKT_TRSV_WIDE_DEDICATED")) nwd = std::atoi(e);
+    ta.nwd = std::max(1, std::min(nwd, ta.nwc));
     // pre-wait bits: 1 fwd narrow, 2 fwd general, 4 bwd narrow, 8 bwd general
     // (poll one value per dependency before loading); with inlined tasks
     // only the general kinds pre-wait, with task calls all of them (r02 A/B)
     ta.pre_wait = c.tr_call ? 15 : 10;
     if (const char* e = std::getenv("HYKKT_TRSV_PREWAIT")) ta.pre_wait = std::atoi(e);
   }
-  ta.nshard = 1;
-  if (const char* e = std::getenv("HYKKT_TRSV_SHARDS")) ta.nshard = std::max(1, std::min(32, std::atoi(e)));
-  ta.tstride = 2 + 32 * ta.nshard;
-  ta.ahead = 0;
+  ta.tstride = 4;  // wide, narrow forward, narrow backward
+  // L1 prefetch in the general tasks (r02 A/B: C4 1036 -> 1022 us per CG
+  // iteration, C1-C3 neutral)
+  ta.prefetch = 1;
+  if (const char* e = std::getenv("HYKKT_TRSV_PREFETCH")) ta.prefetch = std::atoi(e) != 0;
   ta.bt_fill = nullptr;
   ta.bt_rows = c.tr_bt_rows.p;
   ta.nbt_rows = c.tr_nbt_rows;
-  if (const char* e = std::getenv("HYKKT_TRSV_AHEAD")) ta.ahead = std::atoi(e) != 0;
   ta.pos = c.tr_pos.p;
   ta.nbot = c.tr_nbot;
   ta.bot_ptr = c.tr_bot_ptr.p;

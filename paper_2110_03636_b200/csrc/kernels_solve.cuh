@@ -144,15 +144,12 @@ struct TrsvArgs {
   // 1: its rows below)
   const int* chain_fsrc;
   const int* chain_bsrc;
-  // narrow-stream ticket shards: narrow task t belongs to shard t % nshard,
-  // whose counter is ticket[1 + 32 * shard] (one 128-byte line each); a warp
-  // serves shard (narrow warp index) % nshard.  Each shard is a subsequence
-  // of the topological order, so the smallest unfinished task is always
-  // claimed or claimable by its shard's warps: still deadlock-free.  tstride
-  // = counters per pass (k_cg: pass it uses ticket + tstride * it)
-  int nshard;
+  // wide CTAs [0, nwd) serve only the wide stream; [nwd, nwc) are flex
+  // (narrow forward stream first, see trsv_pass); tstride = counters per
+  // pass (k_cg: pass it uses ticket + tstride * it)
+  int nwd;
   int tstride;
-  int ahead;  // narrow stream: claim the next entries while solving the current one
+  int prefetch;  // general tasks: L1 prefetch of their static data before the wait
   // forward right-hand side precomputed in the pass (k_cg): when bt_fill is
   // set, the pass first writes bt_fill[r] = b - J^T u for the rows of every
   // supernode above the bottom levels (bt_rows), alongside bottom level 0,
@@ -359,6 +356,13 @@ __device__ __forceinline__ void fwd_task(const TrsvArgs& a, int sn, int lane, in
   // b - (children's contributions) and for rows below, the running update.
   // (the warp's slice of shared memory when the caller has one and the rows fit)
   double* A = (sA && nr <= kWarpRows) ? sA : a.acc_buf + rp;
+  if (a.prefetch) {  // static data of the extend-add and the panel, into L1 before the wait
+    prefetch_l1(P, 8ll * w * nr, lane);
+    for (int c = s.child_ptr[sn]; c < s.child_ptr[sn + 1]; ++c) {
+      const int ch = s.child[c];
+      prefetch_l1(s.relind + s.u_off[ch], 4ll * (s.nrows[ch] - (s.first[ch + 1] - s.first[ch])), lane);
+    }
+  }
   for (int q = lane; q < nr; q += 32) A[q] = q < w ? rhs_at(a, f + q) : 0.0;
   __syncwarp();
   if (a.pre_wait & 2) wait_children(a, sn, lane);
@@ -513,6 +517,10 @@ __device__ __forceinline__ void bwd_task(const TrsvArgs& a, int sn, int lane, in
     return;
   }
   const int nchunks = (w + 31) >> 5;
+  if (a.prefetch) {  // panel and row indices into L1 before the wait
+    prefetch_l1(P, 8ll * w * nr, lane);
+    prefetch_l1(R, 4ll * nr, lane);
+  }
   for (int ci = nchunks - 1; ci >= 0; --ci) {
     const int cb = ci * 32, cw = min(32, w - cb);
     double d[32];  // column cb+lane of the chunk's diagonal block: L(cb+k, cb+lane)
@@ -1119,13 +1127,21 @@ __device__ __noinline__ void bwd_task_call(const TrsvArgs& a, int sn, int lane, 
 }
 
 // One forward + backward pass; y and x must hold kUnset on entry.
-// Two task streams, each in topological order (forward list, then the same
-// list reversed for the backward pass):
-//   wide supernodes -> CTA tasks on the first `nwc` CTAs (ticket[0]);
-//   narrow ones     -> warp tasks on every warp of the other CTAs (ticket[1]).
-// Both streams follow one global topological order and each is taken in
-// order, so the smallest unfinished task always has its dependencies held by
-// running CTAs / warps: no deadlock.
+// Task streams, each taken in one topological order per pass:
+//   wide supernodes -> CTA tasks (ticket[0]: forward list, then the backward
+//                      list) on the first `nwc` CTAs;
+//   narrow ones     -> warp tasks, forward (ticket[1]) then backward
+//                      (ticket[2]).
+// CTAs: narrow CTAs (index >= nwc) run the narrow forward stream, then the
+// narrow backward stream.  Wide CTAs below `nwd` are dedicated to the wide
+// stream; the other wide CTAs ("flex") first help with the narrow forward
+// stream (their warps would otherwise wait for the top of the tree), then
+// join the wide stream.  Every wide CTA joins the narrow backward stream once
+// the wide stream is exhausted.  Deadlock freedom: a CTA enters the wide
+// stream only after its narrow forward work is done, and the narrow backward
+// stream only after the wide stream has been fully claimed; with at least one
+// dedicated wide CTA, the smallest unfinished task of every stream is held
+// by a CTA / warp that is working on it.
 template <bool CALL>
 __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
   const int tid = threadIdx.x, lane = tid & 31;
@@ -1142,104 +1158,87 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
     grid_sync(a.bar, a.abort);
   }
   if (ps) ps[2] = global_ns();
-  if (static_cast<int>(blockIdx.x) < a.nwc && a.nqf > 0) {
-    // Q-form slices: forward row slices, then backward column slices
-    for (;;) {
-      if (tid == 0) S.task = static_cast<int>(atomicAdd(a.ticket, 1u));
-      __syncthreads();
-      const int t = S.task;
-      __syncthreads();
-      if (t >= a.nqf + a.nqb) break;
-      if (t < a.nqf) {
-        const int4 e = a.qs_f[t];
-        qslice_fwd(a, S, e.x, e.y, e.z);
-      } else {
-        const int4 e = a.qs_b[t - a.nqf];
-        qslice_bwd(a, S, e.x, e.y, e.z);
-      }
-      __syncthreads();
+  const int nt = a.nnar;
+  // one narrow-stream entry: e >= 0 one supernode; e < 0 chain -e - 1 of
+  // single-child narrow supernodes, solved in order by this warp (forward
+  // bottom-up, backward top-down) with no hand-off to another warp
+  auto run_entry = [&](long long t, int e) {
+    const bool fwd = t < nt;
+    const int c0 = e >= 0 ? 0 : a.chain_ptr[-e - 1], cn = e >= 0 ? 1 : a.chain_ptr[-e] - c0;
+    if (CALL && e < 0 && a.chain_fsrc) {  // register hand-off along the chain
+      if (fwd) chain_fwd(a, a.chain_sn + c0, cn, lane);
+      else chain_bwd(a, a.chain_sn + c0, cn, lane);
+      __syncwarp();
+      return;
     }
-  } else if (static_cast<int>(blockIdx.x) < a.nwc) {
-    const int nt = a.nwid;
-    for (;;) {
-      if (tid == 0) S.task = static_cast<int>(atomicAdd(a.ticket, 1u));
-      __syncthreads();
-      const int t = S.task;
-      __syncthreads();
-      if (t >= 2 * nt) break;
-      const bool fwd = t < nt;
-      const int sn = fwd ? a.wid_sn[t] : a.wid_bwd[t - nt];
+    for (int ci = 0; ci < cn; ++ci) {
+      const int sn = e >= 0 ? e : a.chain_sn[c0 + (fwd ? ci : cn - 1 - ci)];
       const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
-      if (a.trace && tid == 0) a.trace[2 * ns + slot] = global_ns();
-      if (fwd) fwd_cta(a, S, sn);
-      else bwd_cta(a, S, sn);
-      if (a.trace && tid == 0) a.trace[slot] = global_ns();
+      if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
+      if (CALL) {
+        if (fwd) fwd_task_call(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+        else bwd_task_call(a, sn, lane, slot);
+      } else {
+        if (fwd) fwd_task<kInlineMid>(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
+        else bwd_task<kInlineMid>(a, sn, lane, slot);
+      }
+      if (a.trace && lane == 0) a.trace[slot] = global_ns();
+      __syncwarp();
+    }
+  };
+  auto narrow_fwd = [&]() {
+    for (long long t = grab_task(a.ticket + 1, lane); t < nt; t = grab_task(a.ticket + 1, lane))
+      run_entry(t, a.nar_sn[t]);
+  };
+  auto narrow_bwd = [&]() {
+    for (long long k = grab_task(a.ticket + 2, lane); k < nt; k = grab_task(a.ticket + 2, lane))
+      run_entry(nt + k, a.nar_bwd[k]);
+  };
+  const bool wide_cta = static_cast<int>(blockIdx.x) < a.nwc;
+  if (!wide_cta) {
+    narrow_fwd();
+    narrow_bwd();
+  } else {
+    if (static_cast<int>(blockIdx.x) >= a.nwd) {
+      narrow_fwd();
       __syncthreads();
     }
-  } else {
-    const int nt = a.nnar;
-    const int nsh = a.nshard;
-    const int shard = (static_cast<int>(blockIdx.x - a.nwc) * static_cast<int>(blockDim.x >> 5) +
-                       static_cast<int>(threadIdx.x >> 5)) % nsh;
-    unsigned* const tk = a.ticket + 1 + 32 * shard;
-    // one narrow-stream entry: e >= 0 one supernode; e < 0 chain -e - 1 of
-    // single-child narrow supernodes, solved in order by this warp (forward
-    // bottom-up, backward top-down) with no hand-off to another warp
-    auto run_entry = [&](long long t, int e) {
-      const bool fwd = t < nt;
-      const int c0 = e >= 0 ? 0 : a.chain_ptr[-e - 1], cn = e >= 0 ? 1 : a.chain_ptr[-e] - c0;
-      if (CALL && e < 0 && a.chain_fsrc) {  // register hand-off along the chain
-        if (fwd) chain_fwd(a, a.chain_sn + c0, cn, lane);
-        else chain_bwd(a, a.chain_sn + c0, cn, lane);
-        __syncwarp();
-        return;
-      }
-      for (int ci = 0; ci < cn; ++ci) {
-        const int sn = e >= 0 ? e : a.chain_sn[c0 + (fwd ? ci : cn - 1 - ci)];
-        const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
-        if (a.trace && lane == 0) a.trace[2 * ns + slot] = global_ns();
-        if (CALL) {
-          if (fwd) fwd_task_call(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
-          else bwd_task_call(a, sn, lane, slot);
+    if (a.nqf > 0) {
+      // Q-form slices: forward row slices, then backward column slices
+      for (;;) {
+        if (tid == 0) S.task = static_cast<int>(atomicAdd(a.ticket, 1u));
+        __syncthreads();
+        const int t = S.task;
+        __syncthreads();
+        if (t >= a.nqf + a.nqb) break;
+        if (t < a.nqf) {
+          const int4 e = a.qs_f[t];
+          qslice_fwd(a, S, e.x, e.y, e.z);
         } else {
-          if (fwd) fwd_task<kInlineMid>(a, sn, lane, slot, S.a + (threadIdx.x >> 5) * kWarpRows);
-          else bwd_task<kInlineMid>(a, sn, lane, slot);
+          const int4 e = a.qs_b[t - a.nqf];
+          qslice_bwd(a, S, e.x, e.y, e.z);
         }
-        if (a.trace && lane == 0) a.trace[slot] = global_ns();
-        __syncwarp();
-      }
-    };
-    const long long tend = 2ll * nt;
-    auto entry_of = [&](long long t) { return t < nt ? a.nar_sn[t] : a.nar_bwd[t - nt]; };
-    if (a.ahead) {
-      // Claims run ahead of the work: the warp holds its current entry, the
-      // next one (ticket resolved, entry index loaded while the current one
-      // is solved) and a claim in flight for the one after, so the ticket
-      // atomic and the entry lookup leave the per-task latency chain.  The
-      // tickets a warp holds increase, so the smallest unfinished entry is
-      // always its holder's current one: still deadlock-free.
-      unsigned r0 = 0, r1 = 0;
-      if (lane == 0) {
-        r0 = atomicAdd(tk, 1u);
-        r1 = atomicAdd(tk, 1u);
-      }
-      long long t = static_cast<long long>(__shfl_sync(0xffffffffu, r0, 0)) * nsh + shard;
-      long long t1 = static_cast<long long>(__shfl_sync(0xffffffffu, r1, 0)) * nsh + shard;
-      int e = t < tend ? entry_of(t) : 0;
-      while (t < tend) {
-        const int e1 = t1 < tend ? entry_of(t1) : 0;
-        unsigned r2 = 0;
-        if (lane == 0 && t1 < tend) r2 = atomicAdd(tk, 1u);
-        run_entry(t, e);
-        const long long t2 = static_cast<long long>(__shfl_sync(0xffffffffu, r2, 0)) * nsh + shard;
-        t = t1;
-        e = e1;
-        t1 = t < tend ? t2 : tend;
+        __syncthreads();
       }
     } else {
-      for (long long t = grab_task(tk, lane) * nsh + shard; t < tend; t = grab_task(tk, lane) * nsh + shard)
-        run_entry(t, entry_of(t));
+      const int nw = a.nwid;
+      for (;;) {
+        if (tid == 0) S.task = static_cast<int>(atomicAdd(a.ticket, 1u));
+        __syncthreads();
+        const int t = S.task;
+        __syncthreads();
+        if (t >= 2 * nw) break;
+        const bool fwd = t < nw;
+        const int sn = fwd ? a.wid_sn[t] : a.wid_bwd[t - nw];
+        const int slot = fwd ? a.pos[sn] : 2 * ns - 1 - a.pos[sn];
+        if (a.trace && tid == 0) a.trace[2 * ns + slot] = global_ns();
+        if (fwd) fwd_cta(a, S, sn);
+        else bwd_cta(a, S, sn);
+        if (a.trace && tid == 0) a.trace[slot] = global_ns();
+        __syncthreads();
+      }
     }
+    narrow_bwd();
   }
   if (ps) ps[3] = global_ns();
   if (a.nbot > 0) {
