@@ -150,6 +150,7 @@ struct hykkt_context {
   hykkt::DBuf<double> cg_bt;  // k_cg: precomputed forward right-hand side (TrsvArgs::bt_fill)
   int tr_nbt_rows = 0;
   int cg_bt_on = 0;
+  unsigned long long* cg_stamps = nullptr;  // diagnostics: 16 per CG CTA (hykkt_debug_cg_phases)
   hykkt::DBuf<unsigned long long> cl_stamps;
   // kb_ruiz_rows: row lists of [[H_tilde, J^T], [J, 0]] (built on first batched solve)
   hykkt::DBuf<int> ruiz_rp, ruiz_ent;
@@ -1114,6 +1115,10 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.bt_fill = nullptr;
   ta.bt_rows = c.tr_bt_rows.p;
   ta.nbt_rows = c.tr_nbt_rows;
+  // every row's right-hand side before the bottom levels (r02 A/B: C4 903 ->
+  // 890 us per CG iteration, C1-C3 -1 %)
+  ta.bt_all = 1;
+  if (const char* e = std::getenv("HYKKT_BT_ALL")) ta.bt_all = std::atoi(e) != 0;
   ta.pos = c.tr_pos.p;
   ta.nbot = c.tr_nbot;
   ta.bot_ptr = c.tr_bot_ptr.p;
@@ -1237,6 +1242,11 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   }
   ensure_qform(c);
   a.tickets = fresh_tickets(c, static_cast<long long>(a.tr.tstride) * (cfg.cg_max_iter + 2));
+  a.cstamp = nullptr;
+  if (c.cg_stamps) {  // diagnostics (hykkt_debug_cg_phases)
+    a.tr.pstamp = c.cg_stamps;
+    a.cstamp = c.cg_stamps + 8 * c.coop_cg_blocks;
+  }
   coop_launch(c, c.tr_call ? (const void*)dev::k_cg<2, true> : c.cg_fn, c.coop_cg_blocks, &a);
   return read_status(c).cg;
 }
@@ -3286,6 +3296,32 @@ int hykkt_debug_trsv_phases(hykkt_t h, uint64_t* out, int64_t cap, int64_t* nblk
                 &ta);
     read_status(c);
     CK(cudaMemcpy(out, st.p, 8 * c.coop_trsv_blocks * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
+// Diagnostics: per-CTA phase times of the last CG iteration of one k_cg run
+// on the current factor and Schur right-hand side (after a solve): 8 per
+// CTA for the pass (as hykkt_debug_trsv_phases), then 8 per CTA for the CG
+// phases (iteration start, pass end, after barrier, J product end, after
+// barrier, x / r end, after barrier).
+int hykkt_debug_cg_phases(hykkt_t h, const hykkt_config_t* cfg, uint64_t* out, int64_t cap, int64_t* nblk) {
+  return guarded([&] {
+    Ctx& c = ctx(h);
+    if (!c.have_factor || !c.have_kkt) throw StateError("needs a factored KKT system");
+    *nblk = c.coop_cg_blocks;
+    if (cap < 16 * c.coop_cg_blocks) return;
+    hykkt::DBuf<unsigned long long> st;
+    st.alloc(16 * c.coop_cg_blocks);
+    CK(cudaMemset(st.p, 0, 16 * c.coop_cg_blocks * sizeof(unsigned long long)));
+    c.cg_stamps = st.p;
+    try {
+      run_cg(c, *cfg, 0.0);
+    } catch (...) {
+      c.cg_stamps = nullptr;
+      throw;
+    }
+    c.cg_stamps = nullptr;
+    CK(cudaMemcpy(out, st.p, 16 * c.coop_cg_blocks * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
 }
 

@@ -158,6 +158,7 @@ struct TrsvArgs {
   double* bt_fill;
   const int* bt_rows;
   int nbt_rows;
+  int bt_all;  // 1: bt_fill covers every row, filled before the bottom levels (one extra grid barrier)
 };
 
 #ifndef HYKKT_INLINE_MID
@@ -190,9 +191,23 @@ __device__ __forceinline__ double rhs_raw(const TrsvArgs& a, int i) {
   const int o = a.s.perm[i];
   double bi = a.rhs.b ? a.rhs.b[o] : 0.0;
   if (a.rhs.u) {
+    // entries four at a time with all their loads in flight, summed in
+    // entry order (the reference's order, bit-identical to one at a time)
     double t = 0.0;
-    for (int q = a.rhs.j_cp[o]; q < a.rhs.j_cp[o + 1]; ++q) {
-      t = __dadd_rn(t, __dmul_rn(a.rhs.jval[q], ldcg(a.rhs.u + a.rhs.j_ri[q])));
+    const int q0 = a.rhs.j_cp[o], q1 = a.rhs.j_cp[o + 1];
+    for (int q = q0; q < q1; q += 4) {
+      int ri[4];
+      double jv[4], uv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ri[k] = q + k < q1 ? __ldg(a.rhs.j_ri + q + k) : 0;
+        jv[k] = q + k < q1 ? __ldg(a.rhs.jval + q + k) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) uv[k] = q + k < q1 ? ldcg(a.rhs.u + ri[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (q + k < q1) t = __dadd_rn(t, __dmul_rn(jv[k], uv[k]));
     }
     bi = a.rhs.b ? __dsub_rn(bi, t) : t;
   }
@@ -837,7 +852,7 @@ __device__ __forceinline__ void fwd_thread(const TrsvArgs& a, int sn) {
   for (int q = 0; q <= NR; ++q) gp[q] = q <= nr ? __ldg(s.gat_ptr + rp + q) : 0;
   double rb[W];
 #pragma unroll
-  for (int q = 0; q < W; ++q) rb[q] = q < w ? rhs_raw(a, f + q) : 0.0;
+  for (int q = 0; q < W; ++q) rb[q] = q < w ? (a.bt_all ? ldcg(a.bt + f + q) : rhs_raw(a, f + q)) : 0.0;
   int i0[NR], i1[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) {
@@ -941,7 +956,7 @@ __device__ __forceinline__ void trsv_bottom(const TrsvArgs& a, bool fwd) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   for (int li = 0; li < a.nbot; ++li) {
     const int l = fwd ? li : a.nbot - 1 - li;
-    if (fwd && li == 0 && a.bt_fill) {
+    if (fwd && li == 0 && a.bt_fill && !a.bt_all) {
       for (int k = gt; k < a.nbt_rows; k += gs) {
         const int r = __ldg(a.bt_rows + k);
         a.bt_fill[r] = rhs_raw(a, r);
@@ -1147,7 +1162,20 @@ __device__ __forceinline__ void trsv_pass(const TrsvArgs& a, TrsvSmem& S) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int ns = a.s.nsup;
   unsigned long long* ps = (a.pstamp && threadIdx.x == 0) ? a.pstamp + 8 * blockIdx.x : nullptr;
-  if (a.nbot > 0) {
+  if (a.bt_fill && a.bt_all) {
+    // every row's right-hand side, two rows per thread in flight
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    const int n = a.s.n;
+    for (int k = gt; k < n; k += 2 * gs) {
+      const int k2 = k + gs;
+      const double v1 = rhs_raw(a, k);
+      const double v2 = k2 < n ? rhs_raw(a, k2) : 0.0;
+      a.bt_fill[k] = v1;
+      if (k2 < n) a.bt_fill[k2] = v2;
+    }
+    grid_sync(a.bar, a.abort);
+    if (a.nbot > 0) trsv_bottom(a, true);
+  } else if (a.nbot > 0) {
     trsv_bottom(a, true);  // fills bt_fill with level 0 (a grid barrier follows)
   } else if (a.bt_fill) {
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
@@ -1280,10 +1308,20 @@ __global__ void k_gather_lrow(int nnz, const int* __restrict__ pos, const double
 __device__ __forceinline__ double j_row_dot(int k, const int* rp, const int* ci_perm,
                                             const double* jcsr, const double* y) {
   double acc = 0.0;
-  for (int e = rp[k]; e < rp[k + 1]; ++e) {
-    const double t = ldcg(y + ci_perm[e]);
-    if (t == 0.0) continue;
-    acc = __dadd_rn(acc, __dmul_rn(jcsr[e], t));
+  const int e0 = rp[k], e1 = rp[k + 1];
+  for (int e = e0; e < e1; e += 4) {  // four entries' loads in flight, summed in order
+    int ci[4];
+    double jv[4], tv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ci[u] = e + u < e1 ? __ldg(ci_perm + e + u) : 0;
+      jv[u] = e + u < e1 ? __ldg(jcsr + e + u) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tv[u] = e + u < e1 ? ldcg(y + ci[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e + u < e1 && tv[u] != 0.0) acc = __dadd_rn(acc, __dmul_rn(jv[u], tv[u]));
   }
   return acc;
 }
@@ -1321,6 +1359,7 @@ struct CgArgs {
   long long max_iter;
   CgResultDev* res;
   unsigned* tickets;  // max_iter + 2 task counters, zeroed
+  unsigned long long* cstamp;  // diagnostics: per-CTA CG phase times (8 per CTA), or null
 };
 
 // Deterministic all-blocks reduction of partials[b * 4 + slot].
@@ -1359,10 +1398,14 @@ __global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
   double rho = rhs_norm * rhs_norm;
   double r_norm = rhs_norm;
   TrsvArgs tr = a.tr;
+  unsigned long long* cs = (a.cstamp && threadIdx.x == 0) ? a.cstamp + 8 * blockIdx.x : nullptr;
   for (long long it = 1; it <= a.max_iter; ++it) {
     tr.ticket = a.tickets + static_cast<long long>(tr.tstride) * it;
+    if (cs) cs[0] = global_ns();
     trsv_pass<CALL>(tr, S);
+    if (cs) cs[1] = global_ns();
     grid_sync(bar, abort);
+    if (cs) cs[2] = global_ns();
     double pq = 0.0, pp = 0.0;
     for (int k = gt; k < a.mc; k += gs) {
       double qk = j_row_dot(k, a.jcsr_rp, a.jcsr_ci_perm, a.jcsr, tr.x);
@@ -1378,7 +1421,9 @@ __global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
       a.partials[blockIdx.x * 4 + 1] = pq;
       a.partials[blockIdx.x * 4 + 2] = pp;
     }
+    if (cs) cs[3] = global_ns();
     grid_sync(bar, abort);
+    if (cs) cs[4] = global_ns();
     const double curvature = reduce_partials(a.partials, 1, scratch);
     const double p_norm2 = reduce_partials(a.partials, 2, scratch);
     if (curvature <= a.thr * p_norm2 || ld_relaxed(abort)) {
@@ -1396,7 +1441,9 @@ __global__ void __launch_bounds__(256, MINB) k_cg(CgArgs a) {
     }
     rr = block_sum(rr, scratch);
     if (threadIdx.x == 0) a.partials[blockIdx.x * 4 + 3] = rr;
+    if (cs) cs[5] = global_ns();
     grid_sync(bar, abort);
+    if (cs) cs[6] = global_ns();
     r_norm = sqrt(reduce_partials(a.partials, 3, scratch));
     const double relres = r_norm / rhs_norm;
     if (relres <= a.tol) {
