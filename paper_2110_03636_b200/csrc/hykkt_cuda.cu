@@ -111,6 +111,7 @@ struct hykkt_context {
   int coop_factor_blocks = 0, coop_trsv_blocks = 0, coop_cg_blocks = 0, coop_ruiz_blocks = 0;
   int coop_bfactor_blocks = 0, coop_btrsv_blocks = 0, coop_bcg_blocks = 0, coop_bruiz_blocks = 0;
   int coop_bruiz_rows_blocks = 0, coop_mf_blocks = 0;
+  int cg_grid = 0, trsv_grid = 0;  // per analysed plan: CTAs of k_cg / k_trsv (<= coop_*_blocks)
   const void* cg_fn = nullptr;
   // multifrontal single-system factor (kernels_mf.cuh)
   hykkt::DBuf<long long> mf_uoff;
@@ -723,6 +724,15 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     // task kind pre-waiting (r02: C1 322 -> 260, C2 392 -> 323, C3 567 -> 544
     // us / CG iteration); larger trees keep them inlined (C4 1553 vs 1897)
     c.tr_call = s.nsup <= 65536 ? 1 : 0;
+    {
+      // solve grids: one CTA per SM for trees up to 16384 supernodes (r02
+      // A/B: C1 197 -> 181, C2 257 -> 249 us per CG iteration: fewer pollers
+      // and cheaper grid barriers), two above
+      int per_sm = s.nsup <= 16384 ? 1 : 2;
+      if (const char* e = std::getenv("HYKKT_SOLVE_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+      c.cg_grid = std::min(c.coop_cg_blocks, per_sm * c.num_sms);
+      c.trsv_grid = std::min(c.coop_trsv_blocks, per_sm * c.num_sms);
+    }
     if (const char* e = std::getenv("HYKKT_TRSV_CALL")) c.tr_call = std::atoi(e) != 0;
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE")) wide = std::max(1ll, std::atoll(e));
     std::vector<int> pos(std::max<idx>(1, s.nsup));
@@ -799,9 +809,20 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     };
     std::vector<int> wid, nar, wid_lev, nar_lev;  // forward order / level order
     for (int sn : fwd_seq) (is_wide(sn) ? wid : nar).push_back(sn);
-    for (idx q = static_cast<idx>(bsn.size()); q < s.nsup; ++q) {
-      const int sn = s.order[q];
-      (is_wide(sn) ? wid_lev : nar_lev).push_back(sn);
+    {
+      // backward lists: reverse level order (descending height), or the
+      // reverse of the forward order (r02 A/B: ACTIVSg10k-sized trees 435 ->
+      // 423 us per CG iteration, the 324k-supernode C4 tree 892 -> 934)
+      const char* e = std::getenv("HYKKT_TRSV_BWD_ORDER");
+      const bool rev_fwd = e ? std::atoi(e) == 1 : (s.nsup > 32768 && s.nsup <= 65536);
+      if (rev_fwd) {
+        for (int sn : fwd_seq) (is_wide(sn) ? wid_lev : nar_lev).push_back(sn);
+      } else {
+        for (idx q = static_cast<idx>(bsn.size()); q < s.nsup; ++q) {
+          const int sn = s.order[q];
+          (is_wide(sn) ? wid_lev : nar_lev).push_back(sn);
+        }
+      }
     }
     // Q-form: every wide supernode (w <= kQMaxW) gets Q = [L_ss^-1; L_below
     // L_ss^-1] after each factorization and runs as independent row /
@@ -1094,7 +1115,7 @@ dev::TrsvArgs trsv_args(Ctx& c) {
     // CTAs reserved for the wide stream (B200 sweep at C2-C4: 48 of 296)
     int nwc = c.q_nsf > 0 ? 96 : 48;  // Q-form slices are independent: more CTAs pay (r02)
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
-    nwc = std::min({nwc, c.tr_nwid, std::max(1, c.coop_cg_blocks / 2)});
+    nwc = std::min({nwc, c.tr_nwid, std::max(1, std::min(c.cg_grid, c.trsv_grid) / 2)});
     ta.nwc = c.tr_nwid > 0 ? nwc : 0;
     // dedicated wide CTAs (the rest of the nwc help with the narrow forward
     // stream first); at least one
@@ -1190,7 +1211,7 @@ void run_trsv(Ctx& c, const double* b, const double* u, const double* jval, doub
     ta.bt = c.cg_bt.p;
   }
   ta.ticket = fresh_tickets(c, ta.tstride);
-  coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
+  coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.trsv_grid,
               &ta);
 }
 
@@ -1245,9 +1266,9 @@ dev::CgResultDev run_cg(Ctx& c, const hykkt_config_t& cfg, double delta2) {
   a.cstamp = nullptr;
   if (c.cg_stamps) {  // diagnostics (hykkt_debug_cg_phases)
     a.tr.pstamp = c.cg_stamps;
-    a.cstamp = c.cg_stamps + 8 * c.coop_cg_blocks;
+    a.cstamp = c.cg_stamps + 8 * c.cg_grid;
   }
-  coop_launch(c, c.tr_call ? (const void*)dev::k_cg<2, true> : c.cg_fn, c.coop_cg_blocks, &a);
+  coop_launch(c, c.tr_call ? (const void*)dev::k_cg<2, true> : c.cg_fn, c.cg_grid, &a);
   return read_status(c).cg;
 }
 
@@ -3282,20 +3303,20 @@ int hykkt_debug_trsv_phases(hykkt_t h, uint64_t* out, int64_t cap, int64_t* nblk
   return guarded([&] {
     Ctx& c = ctx(h);
     if (!c.have_factor || !c.have_kkt) throw StateError("needs a factored KKT system");
-    *nblk = c.coop_trsv_blocks;
-    if (cap < 8 * c.coop_trsv_blocks) return;
+    *nblk = c.trsv_grid;
+    if (cap < 8 * c.trsv_grid) return;
     hykkt::DBuf<unsigned long long> st;
-    st.alloc(8 * c.coop_trsv_blocks);
-    CK(cudaMemset(st.p, 0, 8 * c.coop_trsv_blocks * sizeof(unsigned long long)));
+    st.alloc(8 * c.trsv_grid);
+    CK(cudaMemset(st.p, 0, 8 * c.trsv_grid * sizeof(unsigned long long)));
     ensure_qform(c);
       dev::TrsvArgs ta = trsv_args(c);
     ta.rhs.b = c.rhat.p;
     ta.pstamp = st.p;
     ta.ticket = fresh_tickets(c, ta.tstride);
-    coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
+    coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.trsv_grid,
                 &ta);
     read_status(c);
-    CK(cudaMemcpy(out, st.p, 8 * c.coop_trsv_blocks * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, st.p, 8 * c.trsv_grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
 }
 
@@ -3308,11 +3329,11 @@ int hykkt_debug_cg_phases(hykkt_t h, const hykkt_config_t* cfg, uint64_t* out, i
   return guarded([&] {
     Ctx& c = ctx(h);
     if (!c.have_factor || !c.have_kkt) throw StateError("needs a factored KKT system");
-    *nblk = c.coop_cg_blocks;
-    if (cap < 16 * c.coop_cg_blocks) return;
+    *nblk = c.cg_grid;
+    if (cap < 16 * c.cg_grid) return;
     hykkt::DBuf<unsigned long long> st;
-    st.alloc(16 * c.coop_cg_blocks);
-    CK(cudaMemset(st.p, 0, 16 * c.coop_cg_blocks * sizeof(unsigned long long)));
+    st.alloc(16 * c.cg_grid);
+    CK(cudaMemset(st.p, 0, 16 * c.cg_grid * sizeof(unsigned long long)));
     c.cg_stamps = st.p;
     try {
       run_cg(c, *cfg, 0.0);
@@ -3321,7 +3342,7 @@ int hykkt_debug_cg_phases(hykkt_t h, const hykkt_config_t* cfg, uint64_t* out, i
       throw;
     }
     c.cg_stamps = nullptr;
-    CK(cudaMemcpy(out, st.p, 16 * c.coop_cg_blocks * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, st.p, 16 * c.cg_grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
 }
 
@@ -3359,7 +3380,7 @@ int hykkt_debug_trsv_trace(hykkt_t h, uint64_t* out) {
     ta.rhs.b = c.rhat.p;
     ta.trace = tr.p;
     ta.ticket = fresh_tickets(c, ta.tstride);
-    coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.coop_trsv_blocks,
+    coop_launch(c, c.tr_call ? (const void*)dev::k_trsv<true> : (const void*)dev::k_trsv<false>, c.trsv_grid,
                 &ta);
     read_status(c);
     CK(cudaMemcpy(out, tr.p, 6 * ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
