@@ -1138,6 +1138,10 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.nbt_rows = c.tr_nbt_rows;
   // every row's right-hand side before the bottom levels (r02 A/B: C4 903 ->
   // 890 us per CG iteration, C1-C3 -1 %)
+  // (r02 A/B: C1-C3 -1.3 / -1.9 / -2.5 % per CG iteration; sums regrouped,
+  // <= 1e-13 relative change of the solution)
+  ta.cta_gather = 1;
+  if (const char* e = std::getenv("HYKKT_CTA_GATHER")) ta.cta_gather = std::atoi(e) != 0;
   ta.bt_all = 1;
   if (const char* e = std::getenv("HYKKT_BT_ALL")) ta.bt_all = std::atoi(e) != 0;
   ta.pos = c.tr_pos.p;

@@ -158,7 +158,8 @@ struct TrsvArgs {
   double* bt_fill;
   const int* bt_rows;
   int nbt_rows;
-  int bt_all;  // 1: bt_fill covers every row, filled before the bottom levels (one extra grid barrier)
+  int bt_all;
+  int cta_gather;  // fwd_cta: row-side gathers instead of the per-child extend-add  // 1: bt_fill covers every row, filled before the bottom levels (one extra grid barrier)
 };
 
 #ifndef HYKKT_INLINE_MID
@@ -584,6 +585,16 @@ __device__ void fwd_cta(const TrsvArgs& a, TrsvSmem& S, int sn) {
   const double* P = a.panel + s.off[sn];
   double* U = a.u + s.u_off[sn];
   double* A = S.a;
+  if (a.cta_gather) {
+    // row-side gathers of the children's update values (every row at once,
+    // four loads in flight): no barrier per child
+    const int rp = s.rows_ptr[sn];
+    for (int q = tid; q < nr; q += blockDim.x) {
+      const double g = gather_u(a, __ldg(s.gat_ptr + rp + q), __ldg(s.gat_ptr + rp + q + 1));
+      A[q] = q < w ? rhs_at(a, f + q) - g : g;
+    }
+    __syncthreads();
+  } else {
   for (int q = tid; q < nr; q += blockDim.x) A[q] = q < w ? rhs_at(a, f + q) : 0.0;
   for (int c = s.child_ptr[sn] + tid; c < s.child_ptr[sn + 1]; c += blockDim.x) {
     const int ch = s.child[c];
@@ -601,6 +612,7 @@ __device__ void fwd_cta(const TrsvArgs& a, TrsvSmem& S, int sn) {
       A[q] += (q < w) ? -v : v;
     }
     __syncthreads();
+  }
   }
   for (int cb = 0; cb < w; cb += 32) {
     const int cw = min(32, w - cb);
@@ -723,18 +735,15 @@ __device__ void qslice_fwd(const TrsvArgs& a, TrsvSmem& S, int sn, int r0, int r
   const int f = s.first[sn], w = s.first[sn + 1] - f, nr = s.nrows[sn], rp = s.rows_ptr[sn];
   const double* Q = a.q + a.qoff[sn];
   double* A = S.a;  // w own-row values, then the partial sums
-  for (int qq = tid; qq < w; qq += blockDim.x) {
-    double g = 0.0;
-    for (int e = __ldg(s.gat_ptr + rp + qq), e1 = __ldg(s.gat_ptr + rp + qq + 1); e < e1; ++e)
-      g += load_ready(a.u + __ldg(s.gat_idx + e), a.abort);
-    A[qq] = rhs_at(a, f + qq) - g;
-  }
+  for (int qq = tid; qq < w; qq += blockDim.x)
+    A[qq] = rhs_at(a, f + qq) - gather_u(a, __ldg(s.gat_ptr + rp + qq), __ldg(s.gat_ptr + rp + qq + 1));
   __syncthreads();
   const int q = r0 + lane;
   const bool row = q < r1;
   const int kb = (w * wid) / nwarp, ke = (w * (wid + 1)) / nwarp;
   double t0 = 0.0, t1 = 0.0;
   int k = kb;
+#pragma unroll 4
   for (; k + 2 <= ke; k += 2) {
     if (row) {
       t0 = fma(__ldg(Q + static_cast<long long>(k) * nr + q), A[k], t0);
@@ -751,9 +760,7 @@ __device__ void qslice_fwd(const TrsvArgs& a, TrsvSmem& S, int sn, int r0, int r
     if (q < w) {
       stcg(a.y + f + q, out);
     } else {
-      double g = 0.0;
-      for (int e = __ldg(s.gat_ptr + rp + q), e1 = __ldg(s.gat_ptr + rp + q + 1); e < e1; ++e)
-        g += load_ready(a.u + __ldg(s.gat_idx + e), a.abort);
+      const double g = gather_u(a, __ldg(s.gat_ptr + rp + q), __ldg(s.gat_ptr + rp + q + 1));
       stcg(a.u + s.u_off[sn] + q - w, g + out);
     }
   }
@@ -775,6 +782,7 @@ __device__ void qslice_bwd(const TrsvArgs& a, TrsvSmem& S, int sn, int c0, int c
     const double* Qc = Q + static_cast<long long>(c) * nr;
     double t0 = 0.0, t1 = 0.0;
     int qq = lane;
+#pragma unroll 4
     for (; qq + 32 < nr; qq += 64) {
       t0 = fma(__ldg(Qc + qq), V[qq], t0);
       t1 = fma(__ldg(Qc + qq + 32), V[qq + 32], t1);
