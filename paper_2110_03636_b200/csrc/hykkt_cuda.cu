@@ -323,7 +323,10 @@ const std::size_t kBatchSmem = 8 * static_cast<std::size_t>(batch_smem_rows()) *
 // Supernodes with width * rows >= this (or more rows than a warp's shared
 // accumulator) are solved by a whole CTA in the batched solve.
 long long big_task_wnr() {
-  long long v = 320;  // B200 sweep (batch of 256 ACTIVSg2000, after the update-position change): 12.8 -> 11.5 ms of factor
+  // B200 sweeps on the batch of 256 ACTIVSg2000: 320 in level order (12.8 ->
+  // 11.5 ms of factor); with the depth-ordered job list (r02) 640: 10.8 ->
+  // 8.9 ms (level order at 640: 13.3 ms)
+  long long v = 640;
   if (const char* e = std::getenv("HYKKT_BIG_WNR")) v = std::max(1ll, std::atoll(e));
   return v;
 }
