@@ -722,7 +722,9 @@ void upload_plan(Ctx& c, const CscPattern& src_pattern) {
     // entries, rows within the shared staging buffer) as CTA tasks
     // B200 sweep: smaller trees (C1-C3) gain from more CTA tasks (256 entries),
     // the 324k-supernode C4 tree from keeping the 48 wide CTAs to its top (1024)
-    long long wide = s.nsup <= 65536 ? 256 : 1024;
+    // trees up to 16384 supernodes (one CTA per SM): 512 with 16 wide CTAs
+    // (r02 A/B: ACTIVSg500 179 -> 175, ACTIVSg2000 245 -> 239.5 us per CG iteration)
+    long long wide = s.nsup <= 16384 ? 512 : (s.nsup <= 65536 ? 256 : 1024);
     // trees up to 65536 supernodes (C1-C3): narrow tasks as calls with every
     // task kind pre-waiting (r02: C1 322 -> 260, C2 392 -> 323, C3 567 -> 544
     // us / CG iteration); larger trees keep them inlined (C4 1553 vs 1897)
@@ -1116,7 +1118,7 @@ dev::TrsvArgs trsv_args(Ctx& c) {
   ta.chain_sn = c.tr_chain_sn.p;
   {
     // CTAs reserved for the wide stream (B200 sweep at C2-C4: 48 of 296)
-    int nwc = c.q_nsf > 0 ? 96 : 48;  // Q-form slices are independent: more CTAs pay (r02)
+    int nwc = c.q_nsf > 0 ? 96 : (c.sp.nsup <= 16384 ? 16 : 48);  // Q-form slices are independent: more CTAs pay (r02)
     if (const char* e = std::getenv("HYKKT_TRSV_WIDE_CTAS")) nwc = std::max(1, std::atoi(e));
     nwc = std::min({nwc, c.tr_nwid, std::max(1, std::min(c.cg_grid, c.trsv_grid) / 2)});
     ta.nwc = c.tr_nwid > 0 ? nwc : 0;
